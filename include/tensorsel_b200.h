@@ -1,0 +1,142 @@
+/*
+ * tensorsel_b200.h — C ABI of the B200-native execution path for the
+ * convolution family of tensorsel (arXiv 2512.02371, "HardBoiled").
+ *
+ * The reference (/root/reference/pkg/src/tensorsel) is pure Python; every
+ * entry point below replaces a Python function on its hot path.  The Python
+ * package `paper_2512_02371_b200` binds these with ctypes (see INTEGRATION.md
+ * for the binding a tensorsel maintainer would add).
+ *
+ * Conventions
+ *   - Every call returns a ts_status; ts_last_error() returns a thread-local
+ *     message for the last non-OK status on the calling thread.
+ *   - Device pointers are caller-owned (torch tensors / cudaMalloc); all
+ *     kernels are enqueued on the caller's stream (a cudaStream_t passed as
+ *     void*, NULL = legacy default stream) and never synchronise it.
+ *   - Status codes map 1:1 onto the reference exception classes:
+ *       TS_ERR_OUT_OF_BOUNDS      -> interp.OutOfBounds / layout.OutOfBounds
+ *       TS_ERR_PHASE_MISMATCH     -> layout.PhaseMismatch        (layout.py:24)
+ *       TS_ERR_SHAPE_UNREGISTERED -> interp.ShapeUnregistered     (interp.py:50)
+ *       TS_ERR_UNKNOWN_INTRINSIC  -> interp.UnknownIntrinsic      (interp.py:46)
+ *       TS_ERR_INVALID            -> interp.EvalError             (interp.py:32)
+ */
+#ifndef TENSORSEL_B200_H
+#define TENSORSEL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TS_API __attribute__((visibility("default")))
+#else
+#define TS_API
+#endif
+
+typedef enum ts_status {
+  TS_OK = 0,
+  TS_ERR_INVALID = 1,
+  TS_ERR_OUT_OF_BOUNDS = 2,
+  TS_ERR_PHASE_MISMATCH = 3,
+  TS_ERR_SHAPE_UNREGISTERED = 4,
+  TS_ERR_UNKNOWN_INTRINSIC = 5,
+  TS_ERR_UNSUPPORTED = 6, /* geometry the sm_100a kernels cannot tile        */
+  TS_ERR_CUDA = 7,        /* CUDA runtime / driver error (message has detail) */
+  TS_ERR_NO_DEVICE = 8    /* no sm_100 device visible                         */
+} ts_status;
+
+typedef enum ts_dtype { TS_BF16 = 1, TS_F32 = 2, TS_F16 = 3 } ts_dtype;
+
+/* Axis-builder flags */
+#define TS_AXIS_DC_EXACT 0x1 /* re-balance bf16-rounded taps so every output's taps keep their f32 sum */
+
+/* Opaque handle: one axis of a separable linear transform, i.e. a banded
+ * (n_out x n_in) resampling/filter matrix with clamp-to-edge folded in,
+ * stored on the device as 16-output blocks: a window start per block and a
+ * deduplicated set of bf16 B-operand tiles already in the tcgen05
+ * shared-memory layout.  Built once per (scale, kernel, size) — the
+ * analogue of the reference's hoisted ExprVar weight matrix
+ * (selector.py:309-399, interp.py:214-219). */
+typedef struct ts_axis ts_axis;
+
+typedef struct ts_axis_info {
+  int n_in, n_out;
+  int taps;        /* max taps per output before folding                  */
+  int window;      /* K: input window per 16-output block (multiple of 16) */
+  int blocks;      /* number of 16-output blocks                           */
+  int unique_tiles;/* distinct B tiles after dedup (incl. the zero tile)   */
+  int row_span;    /* input rows one 128-output-row tile reads (pass 1)    */
+  int col_blocks;  /* 16-output blocks per 128-input-column tile (pass 2)  */
+  int col_span;    /* input columns those blocks read (<= 128)             */
+} ts_axis_info;
+
+TS_API const char* ts_last_error(void);
+TS_API int ts_abi_version(void);
+/* number of visible devices with compute capability 10.x; 0 if none */
+TS_API int ts_device_count(void);
+
+/* ---------------------------------------------------------------- builder */
+
+/* General banded axis: output o reads inputs first[o] + t, t < taps, with
+ * weights[o * taps + t]; indices outside [0, n_in) are clamped to the edge
+ * (their weight is folded onto the edge sample).
+ * Replaces layout.matrix_for (layout.py:72-84) + the clamp policy. */
+TS_API ts_status ts_axis_create(int n_in, int n_out, int taps, const int32_t* first,
+                         const float* weights, int flags, int device, ts_axis** out);
+
+/* Axis from a reference ToeplitzSpec (layout.py:32-51): l taps per phase,
+ * stride s (downsample) or p phases (upsample), first tap at input
+ * offset + s*o (p == 1) or offset + o/p (p > 1).  kernel has kernel_len =
+ * p*l entries; TS_ERR_PHASE_MISMATCH otherwise (layout.py:99-102).
+ * Replaces layout.strided_toeplitz / polyphase_toeplitz (layout.py:87-103). */
+TS_API ts_status ts_axis_from_toeplitz(int l, int s, int p, int offset, const float* kernel,
+                                int kernel_len, int n_in, int n_out, int flags, int device,
+                                ts_axis** out);
+
+TS_API ts_status ts_axis_get_info(const ts_axis* a, ts_axis_info* info);
+
+/* Dense (n_out x n_in, row-major, host f32) copy of the effective weights the
+ * device uses (bf16-rounded, edge-folded).  For tests and diagnostics. */
+TS_API ts_status ts_axis_dense(const ts_axis* a, float* out_host);
+
+TS_API void ts_axis_destroy(ts_axis* a);
+
+/* ----------------------------------------------------------- executors */
+
+/* Fused separable transform  out[p] = R · in[p] · Cᵀ  for `planes` planes:
+ * one sm_100a kernel (TMA-staged halo tiles -> tcgen05 vertical pass ->
+ * TMEM -> smem -> tcgen05 horizontal pass -> TMEM -> cast -> TMA store).
+ * in: bf16, out: bf16 or f32.  Strides are in elements; the row stride must
+ * be a multiple of 8 (bf16) / 4 (f32) elements and the plane stride a
+ * multiple of the row stride.  rows->n_in = input height,
+ * cols->n_in = input width. */
+TS_API ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int planes, const void* in,
+                           int64_t in_row_stride, int64_t in_plane_stride, int in_dtype, void* out,
+                           int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
+                           void* stream);
+
+/* Elementwise f32 -> bf16 (round to nearest even), n elements. */
+TS_API ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream);
+
+/* Device-side dense Toeplitz family builder: writes the matrix_rows(spec) x k
+ * row-major matrix of layout.matrix_for (layout.py:72-84) for kernel (device
+ * f32, p*l entries) into out (device f32).  Replaces the Python double loop. */
+TS_API ts_status ts_matrix_for(int l, int k, int s, int p, const float* kernel, float* out, void* stream);
+
+/* Diagnostics: one tcgen05 MMA  D(128 x n) = A(128 x k) · B(k x n)  with A
+ * staged MN-major 128B-swizzled and B K-major interleaved exactly as the
+ * separable kernel stages them.  a: row-major f32 (128 x k), b: row-major
+ * f32 (k x n), d: row-major f32 (128 x n); all device pointers; k % 16 == 0,
+ * n % 16 == 0, n <= 256, k <= 256. */
+TS_API ts_status ts_probe_umma(const float* a, const float* b, float* d, int k, int n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TENSORSEL_B200_H */

@@ -1,0 +1,100 @@
+"""ctypes binding of the sm_100a native library (include/tensorsel_b200.h).
+
+The library is built in-tree (``paper_2512_02371_b200/_native/libtsb200.so``)
+by ``__graft_entry__.build()`` / ``python -m paper_2512_02371_b200.build``.
+There is no fallback: if the library is missing every product entry point
+raises :class:`NativeLibraryMissing`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_native", "libtsb200.so")
+
+TS_BF16, TS_F32, TS_F16 = 1, 2, 3
+TS_AXIS_DC_EXACT = 0x1
+
+_lock = threading.Lock()
+_lib = None
+
+
+class AxisInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "n_in", "n_out", "taps", "window", "blocks", "unique_tiles",
+        "row_span", "col_blocks", "col_span")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_FP = ctypes.POINTER(ctypes.c_float)
+_IP = ctypes.POINTER(ctypes.c_int32)
+
+# name -> (restype, argtypes)
+_SIGNATURES = {
+    "ts_last_error": (ctypes.c_char_p, []),
+    "ts_abi_version": (_I, []),
+    "ts_device_count": (_I, []),
+    "ts_axis_create": (_I, [_I, _I, _I, _IP, _FP, _I, _I, ctypes.POINTER(_P)]),
+    "ts_axis_from_toeplitz": (_I, [_I, _I, _I, _I, _FP, _I, _I, _I, _I, _I,
+                                   ctypes.POINTER(_P)]),
+    "ts_axis_get_info": (_I, [_P, ctypes.POINTER(AxisInfo)]),
+    "ts_axis_dense": (_I, [_P, _FP]),
+    "ts_axis_destroy": (None, [_P]),
+    "ts_separable_run": (_I, [_P, _P, _I, _P, _I64, _I64, _I, _P, _I64, _I64, _I, _P]),
+    "ts_cast_f32_bf16": (_I, [_P, _P, _I64, _P]),
+    "ts_matrix_for": (_I, [_I, _I, _I, _I, _P, _P, _P]),
+    "ts_probe_umma": (_I, [_P, _P, _P, _I, _I, _P]),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+def load(path: str | None = None):
+    """Load (once) and return the native library handle."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise NativeLibraryMissing(
+                f"native library not built: {p} (run `python -m paper_2512_02371_b200.build`)")
+        lib = ctypes.CDLL(p)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.ts_abi_version() != 1:
+            raise NativeLibraryMissing(f"ABI mismatch: library reports {lib.ts_abi_version()}")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().ts_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str = "") -> None:
+    """Raise the reference-compatible exception for a non-OK ts_status."""
+    if status == 0:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    raise errors.from_status(status, msg)

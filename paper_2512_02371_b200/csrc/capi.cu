@@ -1,0 +1,197 @@
+// capi.cu — extern "C" entry points (include/tensorsel_b200.h) plus the small
+// device kernels that sit beside the fused executors: f32->bf16 cast, the
+// device-side dense Toeplitz builder (layout.matrix_for) and a tcgen05
+// descriptor probe used by the parity tests to pin the smem layouts.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "sm100.cuh"
+
+namespace tsb {
+ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const void* in,
+                        int64_t in_rs, int64_t in_ps, int in_dtype, void* out, int64_t out_rs,
+                        int64_t out_ps, int out_dtype, cudaStream_t stream);
+
+// ------------------------------------------------------------------ cast
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                     int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * 8;
+  for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8; i < n;
+       i += stride) {
+    if (i + 8 <= n && ((reinterpret_cast<uintptr_t>(in + i) & 15) == 0) &&
+        ((reinterpret_cast<uintptr_t>(out + i) & 15) == 0)) {
+      float4 a = *reinterpret_cast<const float4*>(in + i);
+      float4 b = *reinterpret_cast<const float4*>(in + i + 4);
+      uint4 o;
+      o.x = pack_bf16x2(a.x, a.y);
+      o.y = pack_bf16x2(a.z, a.w);
+      o.z = pack_bf16x2(b.x, b.y);
+      o.w = pack_bf16x2(b.z, b.w);
+      *reinterpret_cast<uint4*>(out + i) = o;
+    } else {
+      for (int64_t j = i; j < n && j < i + 8; ++j) out[j] = __float2bfloat16_rn(in[j]);
+    }
+  }
+}
+
+// ------------------------------------------------------------ matrix_for
+// out[y][x] = K[tap(y, x)] or 0, tap per layout.kernel_taps (layout.py:60-69)
+__global__ void matrix_for_kernel(int l, int k, int s, int p, int rows,
+                                  const float* __restrict__ kern, float* __restrict__ out) {
+  const int64_t n = static_cast<int64_t>(rows) * k;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int y = static_cast<int>(e / k), x = static_cast<int>(e % k);
+    int tap = -1;
+    if (p > 1) {
+      const int u = y - x / p;
+      if (u >= 0 && u < l) tap = p * u + x % p;
+    } else {
+      const int t = y - s * x;
+      if (t >= 0 && t < l) tap = t;
+    }
+    out[e] = tap >= 0 ? kern[tap] : 0.0f;
+  }
+}
+
+// ------------------------------------------------------------ UMMA probe
+__global__ void __launch_bounds__(128, 1)
+    probe_umma_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                      float* __restrict__ d, int k, int n) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_s = smem_u32(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_s - raw_s);
+  const uint32_t a_bytes = 128u * k * 2u;                   // two 64-wide m-atoms
+  const uint32_t b_bytes = static_cast<uint32_t>(k) * n * 2u;
+  uint8_t* sa = base;
+  uint8_t* sb = base + a_bytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + a_bytes + ((b_bytes + 1023u) & ~1023u));
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const uint32_t lbo_a = static_cast<uint32_t>(k / 8) * 1024u;
+
+  // A (128 x k): MN-major, 128B swizzle — exactly the pass-1 staging layout
+  for (int e = threadIdx.x; e < 128 * k; e += blockDim.x) {
+    const int m = e / k, kk = e % k;
+    const uint32_t off = (m / 64) * lbo_a + (kk / 8) * 1024u + (kk % 8) * 128u +
+                         ((((m % 64) / 8) ^ (kk % 8)) * 16u) + (m % 8) * 2u;
+    *reinterpret_cast<__nv_bfloat16*>(sa + off) = __float2bfloat16_rn(a[e]);
+  }
+  // B (k x n): K-major, no swizzle, 8x8 core matrices
+  for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
+    const int kk = e / n, nn = e % n;
+    const uint32_t off = (nn / 8) * (k * 16u) + (kk / 8) * 128u + (nn % 8) * 16u + (kk % 8) * 2u;
+    *reinterpret_cast<__nv_bfloat16*>(sb + off) = __float2bfloat16_rn(b[e]);
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) tmem_alloc<256>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, n, 1, 0);
+    for (int q = 0; q < k / 16; ++q) {
+      const uint64_t ad = make_sdesc(base_s + q * 2048u, lbo_a, 1024u, kSwizzle128B);
+      const uint64_t bd = make_sdesc(base_s + a_bytes + q * 256u, 128u, k * 16u, kSwizzleNone);
+      mma_f16_ss(tmem, ad, bd, idesc, q > 0 ? 1u : 0u);
+    }
+    mma_commit(bar);
+  }
+  __syncwarp();
+  mbar_wait(bar, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  for (int c0 = 0; c0 < n; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, r);
+    tmem_wait_ld();
+    for (int i = 0; i < 16; ++i) d[row * n + c0 + i] = __uint_as_float(r[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+}  // namespace tsb
+
+using namespace tsb;
+
+extern "C" {
+
+int ts_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int good = 0;
+  for (int d = 0; d < n; ++d) {
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d);
+    if (major == 10) ++good;
+  }
+  return good;
+}
+
+ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int planes, const void* in,
+                           int64_t in_row_stride, int64_t in_plane_stride, int in_dtype, void* out,
+                           int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
+                           void* stream) {
+  return separable_run(rows, cols, planes, in, in_row_stride, in_plane_stride, in_dtype, out,
+                       out_row_stride, out_plane_stride, out_dtype,
+                       static_cast<cudaStream_t>(stream));
+}
+
+ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!in || !out))) return set_error(TS_ERR_INVALID, "cast: bad arguments");
+  if (n == 0) return TS_OK;
+  int64_t blocks = (n / 8 + 255) / 256 + 1;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  cast_f32_bf16_kernel<<<static_cast<int>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      in, static_cast<__nv_bfloat16*>(out), n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "cast kernel launch");
+}
+
+ts_status ts_matrix_for(int l, int k, int s, int p, const float* kernel, float* out,
+                        void* stream) {
+  if (l < 1 || k < 1 || s < 1 || p < 1)
+    return set_error(TS_ERR_INVALID, "ToeplitzSpec needs l, k, s, p >= 1");
+  if (s != 1 && p != 1) return set_error(TS_ERR_INVALID, "stride and phases are exclusive");
+  if (!kernel || !out) return set_error(TS_ERR_INVALID, "matrix_for: null pointer");
+  const int rows = p > 1 ? k / p + l : s * k + l;  // layout.matrix_rows (layout.py:54-57)
+  const int64_t n = static_cast<int64_t>(rows) * k;
+  int blocks = static_cast<int>((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  matrix_for_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(l, k, s, p, rows, kernel,
+                                                                          out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "matrix_for kernel launch");
+}
+
+ts_status ts_probe_umma(const float* a, const float* b, float* d, int k, int n, void* stream) {
+  if (!a || !b || !d || k < 16 || k > 256 || k % 16 || n < 16 || n > 256 || n % 16)
+    return set_error(TS_ERR_INVALID, "probe: need k, n multiples of 16 in [16, 256]");
+  const uint32_t a_bytes = 128u * k * 2u;
+  const uint32_t b_bytes = static_cast<uint32_t>(k) * n * 2u;
+  const uint32_t smem = 1024 + a_bytes + ((b_bytes + 1023u) & ~1023u) + 64;
+  cudaError_t e = cudaFuncSetAttribute(probe_umma_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_error(e, "probe smem attribute");
+  probe_umma_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(a, b, d, k, n);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// common.h — internal types shared by the builder, the C ABI glue and the kernels.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tensorsel_b200.h"
+
+namespace tsb {
+
+// One 16-output block per MMA N-tile.
+constexpr int kBlockN = 16;
+// Extra (ws, tid) entries past the last real block so tiles whose block range
+// overhangs the axis read a harmless zero block (window = last window).
+constexpr int kBlockPad = 64;
+// pass-1 (rows) tile = 8 blocks = 128 output rows = the M of pass 2
+constexpr int kRowBlocksPerTile = 8;
+// pass-1 MMA M = 128 input columns staged per tile
+constexpr int kColTile = 128;
+// TMA boxes are at most 256 rows; a row tile is staged as two boxes
+constexpr int kMaxRowSpan = 512;
+
+// Device-facing view of an axis (passed by value into kernels).
+struct AxisDev {
+  const int32_t* ws;      // window start (input index, multiple of 8) per block
+  const int32_t* tid;     // B-tile id per block (0 = the all-zero tile)
+  const uint8_t* tiles;   // ntiles * tile_bytes, tcgen05 K-major no-swizzle layout
+  int K;                  // window length, multiple of 16
+  int nb;                 // real block count
+  int tile_bytes;         // K * 16 * 2
+};
+
+}  // namespace tsb
+
+struct ts_axis {
+  int n_in = 0, n_out = 0, taps = 0;
+  int K = 0, nb = 0, ntiles = 0, tile_bytes = 0;
+  int row_span = 0;            // rows staged per pass-1 tile (multiple of 16)
+  int col_nbt = 0, col_span = 0;
+  std::vector<int32_t> ws, tid;     // nb + kBlockPad entries
+  std::vector<uint16_t> tiles;      // host copy of the bf16 tiles
+  int device = 0;
+  int32_t* d_ws = nullptr;
+  int32_t* d_tid = nullptr;
+  uint8_t* d_tiles = nullptr;
+
+  tsb::AxisDev dev() const {
+    return tsb::AxisDev{d_ws, d_tid, d_tiles, K, nb, tile_bytes};
+  }
+};
+
+namespace tsb {
+ts_status set_error(ts_status st, const char* fmt, ...);
+ts_status cuda_error(int err, const char* what);
+// Byte offset of element (k, n) inside a K x 16 B tile (K-major, no swizzle:
+// 8x8 core matrices of 128 contiguous bytes; LBO = 128 B between k-chunks,
+// SBO = K*16 B between the two 8-column groups).
+inline int btile_offset(int K, int k, int n) {
+  return (n / 8) * (K * 16) + (k / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+}
+}  // namespace tsb

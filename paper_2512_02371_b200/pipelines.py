@@ -1,0 +1,119 @@
+"""Image pipelines that are linear transforms in disguise, on B200.
+
+The paper's case studies (§V) as one call each, executed by the
+fused sm_100a kernels behind the C ABI:
+
+* :func:`resample` — separable Lanczos-3 resampling (integer or non-integer
+  factor).  ``downsample2x`` is the 2x case of configs 1,
+  2 and 5.
+* :func:`filter_separable`, :func:`gaussian_blur`, :func:`box_blur` —
+  same-size separable convolution (config 3).
+
+Images are planar: a tensor ``(..., H, W)`` is a stack of planes (RGB
+counts as 3 planes).  Inputs are bf16 (or f32, cast to bf16 on the device);
+accumulation is f32 on the tensor cores.  Edges are clamp-to-edge.  There is
+no CPU path: without the native library or a CUDA device these raise.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib, axis as _axis, filters
+from .errors import NoDevice
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _check_device(x):
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise NoDevice("pipelines operate on CUDA tensors; move the image to the GPU first")
+    return x.device.index if x.device.index is not None else torch.cuda.current_device()
+
+
+def _as_planes_bf16(x, stream):
+    """View/copy x (..., H, W) as a (P, H, Wp) bf16 buffer with Wp % 8 == 0."""
+    torch = _torch()
+    H, W = x.shape[-2], x.shape[-1]
+    P = int(np.prod(x.shape[:-2])) if x.dim() > 2 else 1
+    if x.dtype == torch.bfloat16 and W % 8 == 0 and x.is_contiguous():
+        return x.reshape(P, H, W), W
+    Wp = -(-W // 8) * 8
+    if x.dtype == torch.float32 and x.is_contiguous() and W == Wp:
+        buf = torch.empty((P, H, W), dtype=torch.bfloat16, device=x.device)
+        _lib.check(_lib.load().ts_cast_f32_bf16(x.data_ptr(), buf.data_ptr(), x.numel(), stream),
+                   "ts_cast_f32_bf16")
+        return buf, W
+    if x.dtype not in (torch.bfloat16, torch.float32):
+        raise TypeError(f"unsupported input dtype {x.dtype} (bf16 or f32)")
+    buf = torch.zeros((P, H, Wp), dtype=torch.bfloat16, device=x.device)
+    buf[:, :, :W].copy_(x.reshape(P, H, W))
+    return buf, Wp
+
+
+def _run(x, ra, ca, out_dtype):
+    torch = _torch()
+    dev = _check_device(x)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    H, W = x.shape[-2], x.shape[-1]
+    if ra.n_in != H or ca.n_in != W:
+        raise ValueError(f"axes expect {ra.n_in} x {ca.n_in}, image is {H} x {W}")
+    out_dtype = out_dtype or (x.dtype if x.dtype in (torch.bfloat16, torch.float32)
+                              else torch.bfloat16)
+    inb, in_rs = _as_planes_bf16(x, stream)
+    P = inb.shape[0]
+    oh, ow = ra.n_out, ca.n_out
+    align = 8 if out_dtype == torch.bfloat16 else 4
+    owp = -(-ow // align) * align
+    out = torch.empty((P, oh, owp), dtype=out_dtype, device=x.device)
+    ts_out = _lib.TS_BF16 if out_dtype == torch.bfloat16 else _lib.TS_F32
+    _lib.check(_lib.load().ts_separable_run(
+        ra.handle, ca.handle, P, inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16,
+        out.data_ptr(), owp, owp * oh, ts_out, stream), "ts_separable_run")
+    if owp != ow:
+        out = out[:, :, :ow]
+    return out.reshape(*x.shape[:-2], oh, ow)
+
+
+def resample(x, out_h: int, out_w: int, *, out_dtype=None):
+    """Separable Lanczos-3 resample of planar images to (out_h, out_w)."""
+    dev = _check_device(x)
+    H, W = x.shape[-2], x.shape[-1]
+    ra = _axis.lanczos3(H, out_h, dev)
+    ca = _axis.lanczos3(W, out_w, dev)
+    return _run(x, ra, ca, out_dtype)
+
+
+def downsample2x(x, *, out_dtype=None):
+    """Lanczos-3 2x downsample (configs 1/2: 1080p->540p, 4K->1080p)."""
+    H, W = x.shape[-2], x.shape[-1]
+    return resample(x, H // 2, W // 2, out_dtype=out_dtype)
+
+
+def filter_separable(x, kernel_v, kernel_h=None, *, out_dtype=None):
+    """Same-size separable convolution (centred taps, clamp-to-edge)."""
+    dev = _check_device(x)
+    kernel_h = kernel_v if kernel_h is None else kernel_h
+    H, W = x.shape[-2], x.shape[-1]
+    ra = _axis.convolution(H, kernel_v, dev)
+    ca = _axis.convolution(W, kernel_h, dev)
+    return _run(x, ra, ca, out_dtype)
+
+
+def gaussian_blur(x, taps: int, sigma: float | None = None, *, out_dtype=None):
+    k = filters.gaussian_taps(taps, sigma)
+    return filter_separable(x, k, k, out_dtype=out_dtype)
+
+
+def box_blur(x, taps: int, *, out_dtype=None):
+    k = filters.box_taps(taps)
+    return filter_separable(x, k, k, out_dtype=out_dtype)
+
+
+def separable(x, rows: "_axis.Axis", cols: "_axis.Axis", *, out_dtype=None):
+    """Apply explicit axes: out = rows · x · colsᵀ per plane."""
+    return _run(x, rows, cols, out_dtype)
