@@ -120,6 +120,12 @@ TS_API ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int 
                            int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
                            void* stream);
 
+/* Launch geometry ts_separable_run would use for these axes:
+ * out8 = {stages, V buffers, weights resident (0/1), smem bytes, staged rows
+ * per tile, column blocks per tile, tiles, grid CTAs}. */
+TS_API ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes,
+                                   int out_dtype, int* out8);
+
 /* Elementwise f32 -> bf16 (round to nearest even), n elements. */
 TS_API ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream);
 

@@ -13,6 +13,8 @@ namespace tsb {
 ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const void* in,
                         int64_t in_rs, int64_t in_ps, int in_dtype, void* out, int64_t out_rs,
                         int64_t out_ps, int out_dtype, cudaStream_t stream);
+ts_status separable_plan(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype,
+                         int* out8);
 
 // ------------------------------------------------------------------ cast
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -151,6 +153,11 @@ ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int planes,
   return separable_run(rows, cols, planes, in, in_row_stride, in_plane_stride, in_dtype, out,
                        out_row_stride, out_plane_stride, out_dtype,
                        static_cast<cudaStream_t>(stream));
+}
+
+ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes, int out_dtype,
+                            int* out8) {
+  return separable_plan(rows, cols, planes, out_dtype, out8);
 }
 
 ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream) {

@@ -29,6 +29,7 @@ struct AxisDev {
   int K;                  // window length, multiple of 16
   int nb;                 // real block count
   int tile_bytes;         // K * 16 * 2
+  int ntiles;             // distinct tiles (tile 0 is all zeros)
 };
 
 }  // namespace tsb
@@ -46,7 +47,7 @@ struct ts_axis {
   uint8_t* d_tiles = nullptr;
 
   tsb::AxisDev dev() const {
-    return tsb::AxisDev{d_ws, d_tid, d_tiles, K, nb, tile_bytes};
+    return tsb::AxisDev{d_ws, d_tid, d_tiles, K, nb, tile_bytes, ntiles};
   }
 };
 

@@ -6,24 +6,28 @@
 // `wmma_load_a(I, base, s·n, m, k)` / `wmma_load_b(Toeplitz)` / `wmma_mma`
 // statements (rules.py:766-803, interp.py:427-486): an overlapped-window
 // gather times a banded Toeplitz-family matrix, f32 accumulation.  One
-// persistent kernel does both passes of a separable resample / filter:
+// persistent kernel (one CTA per SM) does both passes of a separable
+// resample / filter.  Work unit ("tile") = (plane p, 128 output rows,
+// nb2·16 output columns).  Warp roles:
 //
-//  tile = (plane p, 128 output rows, nb2*16 output columns)
-//  warp 0      TMA producer: input halo tile (R1 rows x 128 cols, bf16,
-//              128B-swizzled) + the block's B tiles (bulk copies) into a
-//              2-stage ring.
-//  warp 1      MMA issuer (one thread):
-//                pass 1 (vertical): for each 16-output-row block k
-//                  D_V[c, 16k..] = Σ_r X[r, c] · R_kᵀ[r, ·]      (M=128 cols, N=16, K=R.K)
-//                  A = staged tile, MN-major SW128; B = R block tile, K-major
-//                pass 2 (horizontal): for each 16-output-column block j
-//                  D_H[i, 16j..] = Σ_c V[i, c] · C_jᵀ[c, ·]      (M=128 rows, N=16, K=C.K)
-//                  A = V (bf16, MN-major SW128, written by the epilogue)
-//  warps 2..5  epilogue: TMEM -> regs -> bf16 -> smem (V operand),
-//              then TMEM -> regs -> cast -> smem -> TMA store.
+//  warp 0      TMA producer: the input halo tile (R1 rows x 128 cols bf16,
+//              128B-swizzled, 4 boxes) into an nst-deep ring; B tiles are
+//              either CTA-resident (copied once) or staged per tile.
+//  warp 1      MMA issuer (one thread), software-pipelined: MMA1(t+1) is
+//              issued before MMA2(t) so the vertical pass of the next tile
+//              overlaps the V-operand epilogue of the current one.
+//                pass 1 (vertical): per 16-output-row block k
+//                  D_V[c, 16k..] = Σ_r X[r, c] · R_kᵀ[r, ·]   M=128 cols, N=16
+//                  A = staged tile (MN-major SW128), B = R tile (K-major)
+//                pass 2 (horizontal): per 16-output-column block j
+//                  D_H[i, 16j..] = Σ_c V[i, c] · C_jᵀ[c, ·]   M=128 rows, N=16
+//                  A = V (bf16 MN-major SW128, written by warps 2-5)
+//  warps 2-5   epilogue 1: D_V (TMEM) -> bf16 -> V operand (smem, x nmid)
+//  warps 6-9   epilogue 2: D_H (TMEM) -> cast -> smem -> TMA store
 //
-// Window starts are multiples of 8 rows/cols (the builder guarantees it) so
-// every MMA operand starts on a 1024-byte swizzle atom.
+// TMEM (512 cols): D_V double-buffered at [0,128) and [128,256), D_H at
+// [256, 256 + nb2·16).  Window starts are multiples of 8 rows/cols (the
+// builder guarantees it) so every MMA operand starts on a 1024-byte atom.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -33,10 +37,22 @@
 
 namespace tsb {
 
-constexpr int kStages = 2;
-constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA, warps 2-5 epilogue
-constexpr uint32_t kTmemCols = 256;
+constexpr int kMaxStages = 4;
+constexpr int kThreads = 320;
+constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kMidBytes = 128 * 128 * 2;  // V tile: 128 rows x 128 cols bf16
+constexpr uint32_t kSmemLimit = 232448;        // max dynamic smem per CTA on sm_100
+
+// Shared-memory plan, chosen on the host and passed to the kernel.
+struct SepSmem {
+  uint32_t nst;        // input stages
+  uint32_t nmid;       // V-operand buffers (1 or 2)
+  uint32_t resident;   // 1: all B tiles copied once; 0: staged with each tile
+  uint32_t in_stage;   // bytes per input stage
+  uint32_t w_stage;    // bytes per weight stage (staged mode)
+  uint32_t w1_bytes;   // offset of the C tiles inside a weight stage / resident block
+  uint32_t off_w, off_mid, off_out, off_bar, total;
+};
 
 struct SepParams {
   AxisDev r;  // rows axis (pass 1)
@@ -44,28 +60,10 @@ struct SepParams {
   int nb2;    // column blocks per tile
   int R1;     // staged input rows per tile (multiple of 16)
   int nrt, nct, planes, ntiles;
-};
-
-struct SepSmem {
-  uint32_t in_stage, w_stage, w1_bytes, out_bytes;
-  uint32_t off_w, off_mid, off_out, off_bar, total;
+  SepSmem L;
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
-
-__host__ __device__ inline SepSmem sep_smem_layout(const SepParams& P, int out_bytes_per_elem) {
-  SepSmem L;
-  L.in_stage = 2u * static_cast<uint32_t>(P.R1) * 128u;
-  L.w1_bytes = static_cast<uint32_t>(kRowBlocksPerTile * P.r.tile_bytes);
-  L.w_stage = align_up(L.w1_bytes + static_cast<uint32_t>(P.nb2 * P.c.tile_bytes), 1024);
-  L.out_bytes = align_up(128u * P.nb2 * 16u * out_bytes_per_elem, 1024);
-  L.off_w = kStages * L.in_stage;
-  L.off_mid = L.off_w + kStages * L.w_stage;
-  L.off_out = L.off_mid + kMidBytes;
-  L.off_bar = L.off_out + L.out_bytes;
-  L.total = L.off_bar + 256 + 1024;  // barriers + alignment slack
-  return L;
-}
 
 template <typename OutT>
 __device__ __forceinline__ void store_out_row(uint32_t dst, const uint32_t (&r)[16]);
@@ -74,7 +72,8 @@ template <>
 __device__ __forceinline__ void store_out_row<__nv_bfloat16>(uint32_t dst, const uint32_t (&r)[16]) {
   uint32_t p[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+  for (int i = 0; i < 8; ++i)
+    p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
   st_shared_v4(dst, p[0], p[1], p[2], p[3]);
   st_shared_v4(dst + 16, p[4], p[5], p[6], p[7]);
 }
@@ -82,10 +81,24 @@ __device__ __forceinline__ void store_out_row<__nv_bfloat16>(uint32_t dst, const
 template <>
 __device__ __forceinline__ void store_out_row<float>(uint32_t dst, const uint32_t (&r)[16]) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) st_shared_v4(dst + 16 * i, r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+  for (int i = 0; i < 4; ++i)
+    st_shared_v4(dst + 16 * i, r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
 }
 
-template <typename OutT>
+struct TileCoord {
+  int p, rt, ct;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const SepParams& P, int t) {
+  TileCoord c;
+  c.ct = t % P.nct;
+  const int rest = t / P.nct;
+  c.rt = rest % P.nrt;
+  c.p = rest / P.nrt;
+  return c;
+}
+
+template <typename OutT, int KQ1, int KQ2>
 __global__ void __launch_bounds__(kThreads, 1)
     separable_kernel(const __grid_constant__ CUtensorMap tm_in,
                      const __grid_constant__ CUtensorMap tm_out, const SepParams P) {
@@ -93,31 +106,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t raw_s = smem_u32(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_s - raw_s);
-  const SepSmem L = sep_smem_layout(P, sizeof(OutT));
+  const SepSmem& L = P.L;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.off_bar);
-  uint64_t* full = bars;                // [kStages] TMA + bulk bytes landed
-  uint64_t* empty = bars + kStages;     // [kStages] tile consumed by both passes
-  uint64_t* dv_full = bars + 2 * kStages;
-  uint64_t* dv_free = dv_full + 1;
-  uint64_t* mid_full = dv_full + 2;
-  uint64_t* dh_full = dv_full + 3;
-  uint64_t* dh_free = dv_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dv_full + 5);
+  uint64_t* full = bars;                      // [kMaxStages] input (+weights) landed
+  uint64_t* empty = bars + kMaxStages;        // [kMaxStages] stage consumed
+  uint64_t* dv_full = bars + 2 * kMaxStages;  // [2]
+  uint64_t* dv_free = dv_full + 2;            // [2]
+  uint64_t* mid_full = dv_full + 4;           // [2]
+  uint64_t* mid_free = dv_full + 6;           // [2]
+  uint64_t* dh_full = dv_full + 8;
+  uint64_t* dh_free = dv_full + 9;
+  uint64_t* wres = dv_full + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dv_full + 11);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(dv_full, 1);
-    mbar_init(dv_free, 128);
-    mbar_init(mid_full, 128);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&dv_full[b], 1);
+      mbar_init(&dv_free[b], 128);
+      mbar_init(&mid_full[b], 128);
+      mbar_init(&mid_free[b], 1);
+    }
     mbar_init(dh_full, 1);
     mbar_init(dh_free, 128);
+    mbar_init(wres, 1);
     fence_barrier_init();
     prefetch_tmap(&tm_in);
     prefetch_tmap(&tm_out);
@@ -128,160 +147,231 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int K1 = P.r.K, K2 = P.c.K;
   const int nb2 = P.nb2;
+  const int nst = static_cast<int>(L.nst);
+  const int nmid = static_cast<int>(L.nmid);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
+      if (L.resident) {
+        const uint32_t rb = static_cast<uint32_t>(P.r.ntiles * P.r.tile_bytes);
+        const uint32_t cb = static_cast<uint32_t>(P.c.ntiles * P.c.tile_bytes);
+        mbar_arrive_expect_tx(wres, rb + cb);
+        bulk_g2s(base + L.off_w, P.r.tiles, rb, wres);
+        bulk_g2s(base + L.off_w + L.w1_bytes, P.c.tiles, cb, wres);
+      }
       const int hr = P.R1 / 2;
       int it = 0;
       for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x, ++it) {
-        const int s = it % kStages;
-        const uint32_t ph = (it / kStages) & 1;
+        const int s = it % nst;
+        const uint32_t ph = (it / nst) & 1;
         mbar_wait(&empty[s], ph ^ 1);
-        const int ct = t % P.nct;
-        const int rest = t / P.nct;
-        const int rt = rest % P.nrt;
-        const int p = rest / P.nrt;
-        const int b1 = rt * kRowBlocksPerTile, b2 = ct * nb2;
+        const TileCoord tc = decode_tile(P, t);
+        const int b1 = tc.rt * kRowBlocksPerTile, b2 = tc.ct * nb2;
         const int row0 = P.r.ws[b1], col0 = P.c.ws[b2];
         uint32_t wbytes = 0;
-        for (int k = 0; k < kRowBlocksPerTile; ++k)
-          if (k == 0 || P.r.tid[b1 + k] != P.r.tid[b1 + k - 1]) wbytes += P.r.tile_bytes;
-        for (int j = 0; j < nb2; ++j)
-          if (j == 0 || P.c.tid[b2 + j] != P.c.tid[b2 + j - 1]) wbytes += P.c.tile_bytes;
+        if (!L.resident) {
+          for (int k = 0; k < kRowBlocksPerTile; ++k)
+            if (k == 0 || P.r.tid[b1 + k] != P.r.tid[b1 + k - 1]) wbytes += P.r.tile_bytes;
+          for (int j = 0; j < nb2; ++j)
+            if (j == 0 || P.c.tid[b2 + j] != P.c.tid[b2 + j - 1]) wbytes += P.c.tile_bytes;
+        }
         mbar_arrive_expect_tx(&full[s], L.in_stage + wbytes);
         uint8_t* dst = base + s * L.in_stage;
-        tma_load_3d(dst, &tm_in, &full[s], col0, row0, p);
-        tma_load_3d(dst + hr * 128, &tm_in, &full[s], col0, row0 + hr, p);
-        tma_load_3d(dst + P.R1 * 128, &tm_in, &full[s], col0 + 64, row0, p);
-        tma_load_3d(dst + P.R1 * 128 + hr * 128, &tm_in, &full[s], col0 + 64, row0 + hr, p);
-        uint8_t* wd = base + L.off_w + s * L.w_stage;
-        for (int k = 0; k < kRowBlocksPerTile; ++k)
-          if (k == 0 || P.r.tid[b1 + k] != P.r.tid[b1 + k - 1])
-            bulk_g2s(wd + k * P.r.tile_bytes,
-                     P.r.tiles + static_cast<size_t>(P.r.tid[b1 + k]) * P.r.tile_bytes,
-                     P.r.tile_bytes, &full[s]);
-        for (int j = 0; j < nb2; ++j)
-          if (j == 0 || P.c.tid[b2 + j] != P.c.tid[b2 + j - 1])
-            bulk_g2s(wd + L.w1_bytes + j * P.c.tile_bytes,
-                     P.c.tiles + static_cast<size_t>(P.c.tid[b2 + j]) * P.c.tile_bytes,
-                     P.c.tile_bytes, &full[s]);
+        tma_load_3d(dst, &tm_in, &full[s], col0, row0, tc.p);
+        tma_load_3d(dst + hr * 128, &tm_in, &full[s], col0, row0 + hr, tc.p);
+        tma_load_3d(dst + P.R1 * 128, &tm_in, &full[s], col0 + 64, row0, tc.p);
+        tma_load_3d(dst + P.R1 * 128 + hr * 128, &tm_in, &full[s], col0 + 64, row0 + hr, tc.p);
+        if (!L.resident) {
+          uint8_t* wd = base + L.off_w + s * L.w_stage;
+          for (int k = 0; k < kRowBlocksPerTile; ++k)
+            if (k == 0 || P.r.tid[b1 + k] != P.r.tid[b1 + k - 1])
+              bulk_g2s(wd + k * P.r.tile_bytes,
+                       P.r.tiles + static_cast<size_t>(P.r.tid[b1 + k]) * P.r.tile_bytes,
+                       P.r.tile_bytes, &full[s]);
+          for (int j = 0; j < nb2; ++j)
+            if (j == 0 || P.c.tid[b2 + j] != P.c.tid[b2 + j - 1])
+              bulk_g2s(wd + L.w1_bytes + j * P.c.tile_bytes,
+                       P.c.tiles + static_cast<size_t>(P.c.tid[b2 + j]) * P.c.tile_bytes,
+                       P.c.tile_bytes, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, /*a MN-major*/ 1, /*b K-major*/ 0);
-      const uint32_t lbo_in = static_cast<uint32_t>(P.R1) * 128u;  // 64-col half stride
-      const uint32_t mid_s = base_s + L.off_mid;
-      int it = 0;
-      for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x, ++it) {
-        const int s = it % kStages;
-        const uint32_t ph = (it / kStages) & 1;
-        const int ct = t % P.nct;
-        const int rt = (t / P.nct) % P.nrt;
-        const int b1 = rt * kRowBlocksPerTile, b2 = ct * nb2;
-        const int row0 = P.r.ws[b1], col0 = P.c.ws[b2];
+    // The whole warp runs this loop (converged); one elected lane issues each
+    // tcgen05 op.  Block tables are fetched lane-parallel (lane k <-> block k)
+    // before the waits so their latency hides behind the pipeline.
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, /*a MN-major*/ 1, /*b K-major*/ 0);
+    const uint32_t lbo_in = static_cast<uint32_t>(P.R1) * 128u;  // 64-col half stride
+    const int kq1 = KQ1 > 0 ? KQ1 : P.r.K / 16;
+    const int kq2 = KQ2 > 0 ? KQ2 : P.c.K / 16;
+    const uint32_t tb1 = P.r.tile_bytes, tb2 = P.c.tile_bytes;
+    const uint32_t sbo1 = static_cast<uint32_t>(P.r.K) * 16u, sbo2 = static_cast<uint32_t>(P.c.K) * 16u;
+    if (L.resident) mbar_wait(wres, 0);
+    for (int it = 0;; ++it) {
+      const int t = blockIdx.x + it * gridDim.x;
+      const bool has = t < P.ntiles;
+      if (has) {
+        // ---- pass 1 of tile `it`
+        const int s = it % nst;
+        const int d = it & 1;
+        const TileCoord tc = decode_tile(P, t);
+        const int b1 = tc.rt * kRowBlocksPerTile;
+        int my_ws = 0, my_tid = 0;
+        if (lane < kRowBlocksPerTile) {
+          my_ws = P.r.ws[b1 + lane];
+          my_tid = P.r.tid[b1 + lane];
+        }
+        const int row0 = __shfl_sync(0xffffffffu, my_ws, 0);
         const uint32_t a0 = base_s + s * L.in_stage;
-        const uint32_t w0 = base_s + L.off_w + s * L.w_stage;
-
-        mbar_wait(&full[s], ph);
-        mbar_wait(dv_free, (it & 1) ^ 1);
+        const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
+        mbar_wait(&full[s], (it / nst) & 1);
+        mbar_wait(&dv_free[d], ((it >> 1) & 1) ^ 1);
+        __syncwarp();
         tc_fence_after();
-        int slot = 0;
+        int slot = 0, prev = -1;
+#pragma unroll
         for (int k = 0; k < kRowBlocksPerTile; ++k) {
-          if (k == 0 || P.r.tid[b1 + k] != P.r.tid[b1 + k - 1]) slot = k;
-          const uint32_t aoff = static_cast<uint32_t>(P.r.ws[b1 + k] - row0) * 128u;
-          for (int q = 0; q < K1 / 16; ++q) {
-            const uint64_t ad = make_sdesc(a0 + aoff + q * 2048u, lbo_in, 1024u, kSwizzle128B);
-            const uint64_t bd =
-                make_sdesc(w0 + slot * P.r.tile_bytes + q * 256u, 128u, K1 * 16u, kSwizzleNone);
-            mma_f16_ss(tmem + 16u * k, ad, bd, idesc, q > 0 ? 1u : 0u);
+          const int wsk = __shfl_sync(0xffffffffu, my_ws, k);
+          const int tidk = __shfl_sync(0xffffffffu, my_tid, k);
+          if (L.resident)
+            slot = tidk;
+          else if (tidk != prev)
+            slot = k;
+          prev = tidk;
+          const uint64_t ad = make_sdesc(a0 + static_cast<uint32_t>(wsk - row0) * 128u, lbo_in,
+                                         1024u, kSwizzle128B);
+          const uint64_t bd = make_sdesc(w0 + slot * tb1, 128u, sbo1, kSwizzleNone);
+          const uint32_t dcol = tmem + d * 128u + 16u * k;
+#pragma unroll
+          for (int q = 0; q < (KQ1 > 0 ? KQ1 : 16); ++q) {
+            if (KQ1 == 0 && q >= kq1) break;
+            // +2048 B (16 rows of A) and +256 B (two k-chunks of B) per K step
+            mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc, q > 0 ? 1u : 0u);
           }
         }
-        mma_commit(dv_full);
-
-        mbar_wait(mid_full, it & 1);
-        mbar_wait(dh_free, (it & 1) ^ 1);
-        tc_fence_after();
-        int slot2 = 0;
-        for (int j = 0; j < nb2; ++j) {
-          if (j == 0 || P.c.tid[b2 + j] != P.c.tid[b2 + j - 1]) slot2 = j;
-          const uint32_t aoff = static_cast<uint32_t>((P.c.ws[b2 + j] - col0) / 8) * 1024u;
-          for (int q = 0; q < K2 / 16; ++q) {
-            const uint64_t ad = make_sdesc(mid_s + aoff + q * 2048u, 16384u, 1024u, kSwizzle128B);
-            const uint64_t bd = make_sdesc(w0 + L.w1_bytes + slot2 * P.c.tile_bytes + q * 256u,
-                                           128u, K2 * 16u, kSwizzleNone);
-            mma_f16_ss(tmem + 128u + 16u * j, ad, bd, idesc, q > 0 ? 1u : 0u);
-          }
-        }
-        mma_commit(dh_full);
-        mma_commit(&empty[s]);
+        mma_commit_elect(&dv_full[d]);
+        if (L.resident) mma_commit_elect(&empty[s]);
       }
+      if (it >= 1) {
+        // ---- pass 2 of tile `it - 1`
+        const int ip = it - 1;
+        const int tp = blockIdx.x + ip * gridDim.x;
+        const int s = ip % nst;
+        const int m = ip % nmid;
+        const TileCoord tc = decode_tile(P, tp);
+        const int b2 = tc.ct * nb2;
+        int my_ws = 0, my_tid = 0;
+        if (lane < nb2) {
+          my_ws = P.c.ws[b2 + lane];
+          my_tid = P.c.tid[b2 + lane];
+        }
+        const int col0 = __shfl_sync(0xffffffffu, my_ws, 0);
+        const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
+        const uint32_t mid_s = base_s + L.off_mid + m * kMidBytes;
+        mbar_wait(&mid_full[m], (ip / nmid) & 1);
+        mbar_wait(dh_free, (ip & 1) ^ 1);
+        __syncwarp();
+        tc_fence_after();
+        int slot = 0, prev = -1;
+#pragma unroll 1
+        for (int j = 0; j < nb2; ++j) {
+          const int wsj = __shfl_sync(0xffffffffu, my_ws, j);
+          const int tidj = __shfl_sync(0xffffffffu, my_tid, j);
+          if (L.resident)
+            slot = tidj;
+          else if (tidj != prev)
+            slot = j;
+          prev = tidj;
+          const uint64_t ad = make_sdesc(mid_s + static_cast<uint32_t>((wsj - col0) / 8) * 1024u,
+                                         16384u, 1024u, kSwizzle128B);
+          const uint64_t bd = make_sdesc(w0 + L.w1_bytes + slot * tb2, 128u, sbo2, kSwizzleNone);
+          const uint32_t dcol = tmem + 256u + 16u * j;
+#pragma unroll
+          for (int q = 0; q < (KQ2 > 0 ? KQ2 : 16); ++q) {
+            if (KQ2 == 0 && q >= kq2) break;
+            mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc, q > 0 ? 1u : 0u);
+          }
+        }
+        mma_commit_elect(dh_full);
+        mma_commit_elect(&mid_free[m]);
+        if (!L.resident) mma_commit_elect(&empty[s]);
+      }
+      if (!has) break;
     }
-  } else {
-    // ------------------------------------------------------------ epilogue
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ epilogue 1
+    const int quarter = warp & 3;       // TMEM lane quarter this warp may access
+    const int c = quarter * 32 + lane;  // input column within the tile
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const uint32_t mid_s = base_s + L.off_mid;
-    const uint32_t out_s = base_s + L.off_out;
-    const uint32_t out_row_bytes = static_cast<uint32_t>(nb2 * 16 * sizeof(OutT));
-    // V operand address pieces for input column c = row
-    const uint32_t mid_row = mid_s + (row / 8) * 1024u + (row % 8) * 128u;
     int it = 0;
     for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x, ++it) {
-      const int ct = t % P.nct;
-      const int rest = t / P.nct;
-      const int rt = rest % P.nrt;
-      const int p = rest / P.nrt;
-
-      // pass-1 accumulator: lane = input column c, column = output row i
-      mbar_wait(dv_full, it & 1);
+      const int d = it & 1;
+      const int m = it % nmid;
+      const uint32_t mid_row =
+          base_s + L.off_mid + m * kMidBytes + (c / 8) * 1024u + (c % 8) * 128u;
+      mbar_wait(&dv_full[d], (it >> 1) & 1);
+      mbar_wait(&mid_free[m], ((it / nmid) & 1) ^ 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int ch = 0; ch < 8; ++ch) {
-        uint32_t r[16];
-        tmem_ld16(t_lane + 16u * ch, r);
-        tmem_wait_ld();
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          const int i8 = ch * 2 + g;  // 8-row group of output rows
-          const uint32_t addr = mid_row + (i8 / 8) * 16384u + (((i8 % 8) ^ (row % 8)) * 16u);
-          st_shared_v4(addr,
-                       pack_bf16x2(__uint_as_float(r[8 * g + 0]), __uint_as_float(r[8 * g + 1])),
-                       pack_bf16x2(__uint_as_float(r[8 * g + 2]), __uint_as_float(r[8 * g + 3])),
-                       pack_bf16x2(__uint_as_float(r[8 * g + 4]), __uint_as_float(r[8 * g + 5])),
-                       pack_bf16x2(__uint_as_float(r[8 * g + 6]), __uint_as_float(r[8 * g + 7])));
+      for (int h = 0; h < 2; ++h) {
+        uint32_t r[4][16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tmem_ld16(t_lane + d * 128u + 64u * h + 16u * q, r[q]);
+        tmem_wait_ld();
+        if (h == 1) {
+          tc_fence_before();
+          mbar_arrive(&dv_free[d]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const int i8 = h * 8 + q * 2 + g;  // 8-row group of output rows
+            const uint32_t addr = mid_row + (i8 / 8) * 16384u + (((i8 % 8) ^ (c % 8)) * 16u);
+            st_shared_v4(addr,
+                         pack_bf16x2(__uint_as_float(r[q][8 * g + 0]), __uint_as_float(r[q][8 * g + 1])),
+                         pack_bf16x2(__uint_as_float(r[q][8 * g + 2]), __uint_as_float(r[q][8 * g + 3])),
+                         pack_bf16x2(__uint_as_float(r[q][8 * g + 4]), __uint_as_float(r[q][8 * g + 5])),
+                         pack_bf16x2(__uint_as_float(r[q][8 * g + 6]), __uint_as_float(r[q][8 * g + 7])));
+          }
         }
       }
-      tc_fence_before();
-      mbar_arrive(dv_free);
       fence_proxy_async_smem();
-      mbar_arrive(mid_full);
-
-      // pass-2 accumulator: lane = output row i, column = output column j
+      mbar_arrive(&mid_full[m]);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue 2
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;  // output row within the tile
+    const int et = threadIdx.x - 192;     // 0..127
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + 256u;
+    const uint32_t out_row_bytes = static_cast<uint32_t>(nb2 * 16 * sizeof(OutT));
+    const uint32_t orow = base_s + L.off_out + row * out_row_bytes;
+    int it = 0;
+    for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x, ++it) {
+      const TileCoord tc = decode_tile(P, t);
       mbar_wait(dh_full, it & 1);
       tc_fence_after();
-      if (et == 0) bulk_wait_read0();  // previous TMA store finished reading staging
-      named_bar_sync(1, 128);
-      const uint32_t orow = out_s + row * out_row_bytes;
-#pragma unroll 1
-      for (int j = 0; j < nb2; ++j) {
-        uint32_t r[16];
-        tmem_ld16(t_lane + 128u + 16u * j, r);
-        tmem_wait_ld();
-        store_out_row<OutT>(orow + j * 16u * sizeof(OutT), r);
-      }
+      uint32_t r[8][16];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < nb2) tmem_ld16(t_lane + 16u * j, r[j]);
+      tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(dh_free);
+      if (et == 0) bulk_wait_read0();  // previous TMA store finished reading staging
+      named_bar_sync(2, 128);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < nb2) store_out_row<OutT>(orow + j * 16u * sizeof(OutT), r[j]);
       fence_proxy_async_smem();
-      named_bar_sync(1, 128);
+      named_bar_sync(2, 128);
       if (et == 0) {
-        tma_store_3d(&tm_out, base + L.off_out, ct * nb2 * 16, rt * kRowBlocksPerTile * 16, p);
+        tma_store_3d(&tm_out, base + L.off_out, tc.ct * nb2 * 16, tc.rt * kRowBlocksPerTile * 16,
+                     tc.p);
         bulk_commit();
       }
     }
@@ -346,19 +436,101 @@ int sm_count_current() {
   return n > 0 ? n : 148;
 }
 
+// Pick stages / V buffers / weight residency to fit the shared-memory budget,
+// preferring (in order) two V buffers, resident weights, then more stages.
+static bool plan_smem(SepParams& P, int oes) {
+  const uint32_t in_stage = 2u * static_cast<uint32_t>(P.R1) * 128u;
+  const uint32_t tb1 = P.r.tile_bytes, tb2 = P.c.tile_bytes;
+  const uint32_t res_w1 = align_up(static_cast<uint32_t>(P.r.ntiles) * tb1, 128);
+  const uint32_t res_bytes = align_up(res_w1 + static_cast<uint32_t>(P.c.ntiles) * tb2, 1024);
+  const uint32_t st_w1 = kRowBlocksPerTile * tb1;
+  const uint32_t st_bytes = align_up(st_w1 + P.nb2 * tb2, 1024);
+  const uint32_t out_bytes = align_up(128u * P.nb2 * 16u * oes, 1024);
+  const uint32_t fixed = out_bytes + 256 + 1024;  // barriers + alignment slack
+  for (uint32_t nmid = 2; nmid >= 1; --nmid) {
+    for (int resident = 1; resident >= 0; --resident) {
+      for (uint32_t nst = kMaxStages; nst >= 2; --nst) {
+        const uint32_t wb = resident ? res_bytes : nst * st_bytes;
+        const uint32_t total = nst * in_stage + wb + nmid * kMidBytes + fixed;
+        if (total > kSmemLimit) continue;
+        SepSmem& L = P.L;
+        L.nst = nst;
+        L.nmid = nmid;
+        L.resident = static_cast<uint32_t>(resident);
+        L.in_stage = in_stage;
+        L.w_stage = st_bytes;
+        L.w1_bytes = resident ? res_w1 : st_w1;
+        L.off_w = nst * in_stage;
+        L.off_mid = L.off_w + wb;
+        L.off_out = L.off_mid + nmid * kMidBytes;
+        L.off_bar = L.off_out + out_bytes;
+        L.total = L.off_bar + 256 + 1024;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
+template <typename OutT, int KQ1, int KQ2>
+static ts_status launch_sep_k(const SepParams& P, const CUtensorMap& tin, const CUtensorMap& tout,
+                              cudaStream_t stream) {
+  auto kern = separable_kernel<OutT, KQ1, KQ2>;
+  // per-device attribute; cheap, so set it on every launch
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(P.L.total));
+  if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(separable smem)");
+  const int sms = sm_count_current();
+  const int grid = P.ntiles < sms ? P.ntiles : sms;
+  kern<<<grid, kThreads, P.L.total, stream>>>(tin, tout, P);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_error(e, "separable_kernel launch");
+  return TS_OK;
+}
+
+// Compile-time K-step counts for the common windows (32, 48, 64 inputs per
+// 16-output block); anything else runs the runtime-count variant.
+template <typename OutT, int KQ1>
+static ts_status launch_sep_k2(const SepParams& P, const CUtensorMap& tin,
+                               const CUtensorMap& tout, cudaStream_t stream) {
+  switch (P.c.K / 16) {
+    case 2: return launch_sep_k<OutT, KQ1, 2>(P, tin, tout, stream);
+    case 3: return launch_sep_k<OutT, KQ1, 3>(P, tin, tout, stream);
+    case 4: return launch_sep_k<OutT, KQ1, 4>(P, tin, tout, stream);
+    default: return launch_sep_k<OutT, KQ1, 0>(P, tin, tout, stream);
+  }
+}
+
 template <typename OutT>
 static ts_status launch_sep(const SepParams& P, const CUtensorMap& tin, const CUtensorMap& tout,
                             cudaStream_t stream) {
-  const SepSmem L = sep_smem_layout(P, sizeof(OutT));
-  // per-device attribute; cheap, so set it on every launch
-  cudaError_t e = cudaFuncSetAttribute(separable_kernel<OutT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(L.total));
-  if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(separable smem)");
-  const int grid = P.ntiles < sm_count_current() ? P.ntiles : sm_count_current();
-  separable_kernel<OutT><<<grid, kThreads, L.total, stream>>>(tin, tout, P);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_error(e, "separable_kernel launch");
+  switch (P.r.K / 16) {
+    case 2: return launch_sep_k2<OutT, 2>(P, tin, tout, stream);
+    case 3: return launch_sep_k2<OutT, 3>(P, tin, tout, stream);
+    case 4: return launch_sep_k2<OutT, 4>(P, tin, tout, stream);
+    default: return launch_sep_k2<OutT, 0>(P, tin, tout, stream);
+  }
+}
+
+static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, int oes,
+                             SepParams& P) {
+  if (ra->row_span > kMaxRowSpan || ra->row_span % 16)
+    return set_error(TS_ERR_UNSUPPORTED, "rows axis: row tile span %d > %d", ra->row_span,
+                     kMaxRowSpan);
+  if (ca->col_nbt < 1)
+    return set_error(TS_ERR_UNSUPPORTED, "cols axis: window %d does not fit a 128-column tile",
+                     ca->K);
+  P.r = ra->dev();
+  P.c = ca->dev();
+  P.nb2 = ca->col_nbt;
+  P.R1 = ra->row_span;
+  P.nrt = (ra->nb + kRowBlocksPerTile - 1) / kRowBlocksPerTile;
+  P.nct = (ca->nb + P.nb2 - 1) / P.nb2;
+  P.planes = planes;
+  P.ntiles = planes * P.nrt * P.nct;
+  if (!plan_smem(P, oes))
+    return set_error(TS_ERR_UNSUPPORTED, "separable: tile (R1=%d, nb2=%d) does not fit smem",
+                     P.R1, P.nb2);
   return TS_OK;
 }
 
@@ -372,12 +544,6 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   if (out_dtype != TS_BF16 && out_dtype != TS_F32)
     return set_error(TS_ERR_UNSUPPORTED, "separable: output must be bf16 or f32");
   const int oes = out_dtype == TS_BF16 ? 2 : 4;
-  if (ra->row_span > kMaxRowSpan || ra->row_span % 16)
-    return set_error(TS_ERR_UNSUPPORTED, "rows axis: row tile span %d > %d", ra->row_span,
-                     kMaxRowSpan);
-  if (ca->col_nbt < 1)
-    return set_error(TS_ERR_UNSUPPORTED, "cols axis: window %d does not fit a 128-column tile",
-                     ca->K);
   if (in_rs < ca->n_in || (in_rs * 2) % 16 || in_ps < in_rs * ra->n_in || (in_ps * 2) % 16)
     return set_error(TS_ERR_INVALID, "separable: input strides (%lld, %lld) invalid for %d x %d",
                      (long long)in_rs, (long long)in_ps, ra->n_in, ca->n_in);
@@ -385,7 +551,6 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
       (out_ps * oes) % 16)
     return set_error(TS_ERR_INVALID, "separable: output strides (%lld, %lld) invalid for %d x %d",
                      (long long)out_rs, (long long)out_ps, ra->n_out, ca->n_out);
-
   if (ra->device != ca->device)
     return set_error(TS_ERR_INVALID, "separable: axes live on devices %d and %d", ra->device,
                      ca->device);
@@ -393,18 +558,11 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
 
   SepParams P;
-  P.r = ra->dev();
-  P.c = ca->dev();
-  P.nb2 = ca->col_nbt;
-  P.R1 = ra->row_span;
-  P.nrt = (ra->nb + kRowBlocksPerTile - 1) / kRowBlocksPerTile;
-  P.nct = (ca->nb + P.nb2 - 1) / P.nb2;
-  P.planes = planes;
-  P.ntiles = planes * P.nrt * P.nct;
-
+  ts_status st = make_params(ra, ca, planes, oes, P);
+  if (st != TS_OK) return st;
   CUtensorMap tin, tout;
-  ts_status st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, ca->n_in, ra->n_in,
-                                planes, in_rs, in_ps, 64, P.R1 / 2, CU_TENSOR_MAP_SWIZZLE_128B);
+  st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, ca->n_in, ra->n_in, planes,
+                      in_rs, in_ps, 64, P.R1 / 2, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TS_OK) return st;
   st = encode_tmap_3d(&tout,
                       out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -412,11 +570,26 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
                       oes, out, ca->n_out, ra->n_out, planes, out_rs, out_ps, P.nb2 * 16, 128,
                       CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TS_OK) return st;
-  const SepSmem L = sep_smem_layout(P, oes);
-  if (L.total > 232448u)
-    return set_error(TS_ERR_UNSUPPORTED, "separable: %u bytes of shared memory needed", L.total);
   if (out_dtype == TS_BF16) return launch_sep<__nv_bfloat16>(P, tin, tout, stream);
   return launch_sep<float>(P, tin, tout, stream);
+}
+
+// The launch geometry a run would use (ts_separable_plan).
+ts_status separable_plan(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype,
+                         int* out8) {
+  if (!ra || !ca || !out8) return set_error(TS_ERR_INVALID, "separable_plan: null argument");
+  SepParams P;
+  ts_status st = make_params(ra, ca, planes < 1 ? 1 : planes, out_dtype == TS_BF16 ? 2 : 4, P);
+  if (st != TS_OK) return st;
+  out8[0] = static_cast<int>(P.L.nst);
+  out8[1] = static_cast<int>(P.L.nmid);
+  out8[2] = static_cast<int>(P.L.resident);
+  out8[3] = static_cast<int>(P.L.total);
+  out8[4] = P.R1;
+  out8[5] = P.nb2;
+  out8[6] = P.ntiles;
+  out8[7] = P.ntiles < sm_count_current() ? P.ntiles : sm_count_current();
+  return TS_OK;
 }
 
 }  // namespace tsb
