@@ -1,0 +1,117 @@
+"""Image-level pipelines restated on the CPU (numpy, f32).
+
+TEST INFRASTRUCTURE ONLY.  Built from the reference's tile semantics: every
+1-D pass is the source-form conv statement of make_corpus.conv_update
+(tools/make_corpus.py:142-150) evaluated as interp does — f32 products,
+taps summed left to right (interp.py:162-167, 203-211), then ``+ acc`` with
+acc = 0 (the Store of ``conv``).  tests/golden/ pins that 1-D pass
+bit-exactly against interp.run_program on generated tile programs.
+
+What the reference does not define is restated from the paper and chosen
+here (parity unpinned, documented in DESIGN.md):
+  * Lanczos-3 kernel sinc(x)·sinc(x/3), |x| < 3, output o at
+    input coordinate (o + 0.5)·f − 0.5, stretched by max(f, 1), normalised;
+  * Gaussian sigma = taps/6 and box 1/taps, centred taps;
+  * clamp-to-edge at image borders;
+  * separable order: horizontal pass, then vertical (either order is the
+    same linear map; only f32 rounding differs);
+  * DCT-16 denoise: see dct_denoise.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+# ------------------------------------------------------------------ weights
+def _sinc(x):
+    if x == 0.0:
+        return 1.0
+    return math.sin(math.pi * x) / (math.pi * x)
+
+
+def lanczos3_weights(n_in, n_out):
+    """(first[n_out], weights[n_out, taps]) for Lanczos-3 resampling."""
+    f = n_in / n_out
+    fs = max(f, 1.0)
+    rows = []
+    for o in range(n_out):
+        c = (o + 0.5) * f - 0.5
+        lo = math.ceil(c - 3.0 * fs - 1e-9)
+        hi = math.floor(c + 3.0 * fs + 1e-9)
+        w = []
+        for j in range(lo, hi + 1):
+            x = (j - c) / fs
+            w.append(_sinc(x) * _sinc(x / 3.0) if abs(x) < 3.0 else 0.0)
+        s = sum(w)
+        rows.append((lo, [v / s for v in w]))
+    taps = max(len(w) for _, w in rows)
+    first = np.array([lo for lo, _ in rows], np.int64)
+    weights = np.zeros((n_out, taps), np.float32)
+    for o, (_, w) in enumerate(rows):
+        weights[o, :len(w)] = np.asarray(w, np.float64).astype(np.float32)
+    return first, weights
+
+
+def gaussian_kernel(taps, sigma=None):
+    sigma = taps / 6.0 if sigma is None else sigma
+    h = (taps - 1) / 2.0
+    w = [math.exp(-0.5 * ((t - h) / sigma) ** 2) for t in range(taps)]
+    s = sum(w)
+    return np.array([v / s for v in w], np.float64).astype(np.float32)
+
+
+def box_kernel(taps):
+    return np.full(taps, 1.0 / taps, np.float32)
+
+
+def centred_axis(n, kernel):
+    kernel = np.asarray(kernel, np.float32)
+    taps = len(kernel)
+    first = np.arange(n) - (taps - 1) // 2
+    return first.astype(np.int64), np.tile(kernel, (n, 1))
+
+
+# ------------------------------------------------------------------ passes
+def axis_pass(x, first, weights, axis):
+    """One 1-D pass along `axis`: out[..., o] = (Σ_t x[..., clamp(first[o]+t)]
+    · w[o, t]) + 0, f32, t left to right."""
+    x = np.moveaxis(np.asarray(x, np.float32), axis, -1)
+    n_in = x.shape[-1]
+    first = np.asarray(first, np.int64)
+    weights = np.asarray(weights, np.float32)
+    acc = None
+    for t in range(weights.shape[1]):
+        idx = np.clip(first + t, 0, n_in - 1)
+        term = (x[..., idx] * weights[:, t]).astype(np.float32)
+        acc = term if acc is None else (acc + term).astype(np.float32)
+    acc = (acc + np.float32(0.0)).astype(np.float32)
+    return np.moveaxis(acc, -1, axis)
+
+
+def separable(img, rows, cols):
+    """Horizontal pass then vertical pass; rows/cols = (first, weights)."""
+    h = axis_pass(img, cols[0], cols[1], axis=-1)
+    return axis_pass(h, rows[0], rows[1], axis=-2)
+
+
+def resample(img, out_h, out_w):
+    img = np.asarray(img, np.float32)
+    H, W = img.shape[-2:]
+    return separable(img, lanczos3_weights(H, out_h), lanczos3_weights(W, out_w))
+
+
+def gaussian_blur(img, taps, sigma=None):
+    img = np.asarray(img, np.float32)
+    k = gaussian_kernel(taps, sigma)
+    H, W = img.shape[-2:]
+    return separable(img, centred_axis(H, k), centred_axis(W, k))
+
+
+def box_blur(img, taps):
+    img = np.asarray(img, np.float32)
+    k = box_kernel(taps)
+    H, W = img.shape[-2:]
+    return separable(img, centred_axis(H, k), centred_axis(W, k))

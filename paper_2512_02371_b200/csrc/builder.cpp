@@ -68,24 +68,35 @@ void dc_rebalance(std::vector<uint16_t>& col_bits, const std::vector<double>& co
   if (order.empty() || got == target) return;
   std::sort(order.begin(), order.end(),
             [&](int a, int b) { return std::fabs(col_w[a]) > std::fabs(col_w[b]); });
-  for (int i : order) {
-    const uint16_t base = col_bits[i];
-    const double base_v = bf16_bits_to_f32(base);
+  // Greedy: each round take the single one-ulp step (on any tap, at most two
+  // ulps from its rounded value) that most reduces the sum error; ties go to
+  // the larger tap.  Stops when no step helps.
+  std::vector<int> moved(col_bits.size(), 0);
+  for (int round = 0; round < 64 && got != target; ++round) {
     double best_err = std::fabs(got - target);
-    uint16_t best = base;
-    for (int d = -1; d <= 1; d += 2) {
-      const int mag = static_cast<int>(base & 0x7FFF) + d;
-      if (mag <= 0 || mag >= 0x7F80) continue;  // never flip sign or reach inf
-      const uint16_t cand = static_cast<uint16_t>((base & 0x8000) | mag);
-      const double err = std::fabs(got - base_v + bf16_bits_to_f32(cand) - target);
-      if (err < best_err) {
-        best_err = err;
-        best = cand;
+    int best_i = -1, best_d = 0;
+    uint16_t best_bits = 0;
+    for (int i : order) {
+      for (int d = -1; d <= 1; d += 2) {
+        if (std::abs(moved[i] + d) > 2) continue;
+        const uint16_t b = col_bits[i];
+        const int mag = static_cast<int>(b & 0x7FFF) + d;
+        if (mag <= 0 || mag >= 0x7F80) continue;  // never flip sign or reach inf
+        const uint16_t cand = static_cast<uint16_t>((b & 0x8000) | mag);
+        const double err =
+            std::fabs(got - bf16_bits_to_f32(b) + bf16_bits_to_f32(cand) - target);
+        if (err < best_err) {
+          best_err = err;
+          best_i = i;
+          best_d = d;
+          best_bits = cand;
+        }
       }
     }
-    got += bf16_bits_to_f32(best) - base_v;
-    col_bits[i] = best;
-    if (got == target) break;
+    if (best_i < 0) break;
+    got += static_cast<double>(bf16_bits_to_f32(best_bits)) - bf16_bits_to_f32(col_bits[best_i]);
+    col_bits[best_i] = best_bits;
+    moved[best_i] += best_d;
   }
 }
 }  // namespace
