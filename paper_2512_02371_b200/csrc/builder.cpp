@@ -207,6 +207,12 @@ static ts_status build_axis_host(int n_in, int n_out, int taps, const int32_t* f
     a->ws[b] = ws[b];
     a->tid[b] = tid[b];
   }
+  if (a->ws[0] < -32768 || a->ws[nb - 1] > 32767 || a->ntiles > 65535)
+    return set_error(TS_ERR_UNSUPPORTED, "axis too long for packed block tables");
+  a->tab.resize(a->ws.size());
+  for (size_t b = 0; b < a->ws.size(); ++b)
+    a->tab[b] = static_cast<int32_t>(static_cast<uint32_t>(a->ws[b]) << 16) |
+                static_cast<int32_t>(a->tid[b] & 0xFFFF);
 
   // pass-1 (rows) geometry: 8 blocks per tile
   int rspan = 0;
@@ -241,11 +247,14 @@ static ts_status upload_axis(ts_axis* a, int device) {
   ts_status st = TS_OK;
   if ((e = cudaMalloc(&a->d_ws, nbp * 4)) != cudaSuccess ||
       (e = cudaMalloc(&a->d_tid, nbp * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&a->d_tab, nbp * 4)) != cudaSuccess ||
       (e = cudaMalloc(&a->d_tiles, a->tiles.size() * 2)) != cudaSuccess) {
     st = cuda_error(e, "cudaMalloc(axis)");
   } else if ((e = cudaMemcpy(a->d_ws, a->ws.data(), nbp * 4, cudaMemcpyHostToDevice)) !=
                  cudaSuccess ||
              (e = cudaMemcpy(a->d_tid, a->tid.data(), nbp * 4, cudaMemcpyHostToDevice)) !=
+                 cudaSuccess ||
+             (e = cudaMemcpy(a->d_tab, a->tab.data(), nbp * 4, cudaMemcpyHostToDevice)) !=
                  cudaSuccess ||
              (e = cudaMemcpy(a->d_tiles, a->tiles.data(), a->tiles.size() * 2,
                              cudaMemcpyHostToDevice)) != cudaSuccess) {
@@ -269,6 +278,7 @@ void ts_axis_destroy(ts_axis* a) {
   if (!a) return;
   if (a->d_ws) cudaFree(a->d_ws);
   if (a->d_tid) cudaFree(a->d_tid);
+  if (a->d_tab) cudaFree(a->d_tab);
   if (a->d_tiles) cudaFree(a->d_tiles);
   delete a;
 }

@@ -25,6 +25,7 @@ constexpr int kMaxRowSpan = 512;
 struct AxisDev {
   const int32_t* ws;      // window start (input index, multiple of 8) per block
   const int32_t* tid;     // B-tile id per block (0 = the all-zero tile)
+  const int32_t* tab;     // packed per block: (ws << 16) | tid
   const uint8_t* tiles;   // ntiles * tile_bytes, tcgen05 K-major no-swizzle layout
   int K;                  // window length, multiple of 16
   int nb;                 // real block count
@@ -44,10 +45,12 @@ struct ts_axis {
   int device = 0;
   int32_t* d_ws = nullptr;
   int32_t* d_tid = nullptr;
+  int32_t* d_tab = nullptr;
   uint8_t* d_tiles = nullptr;
+  std::vector<int32_t> tab;         // packed (ws << 16) | tid, nb + kBlockPad entries
 
   tsb::AxisDev dev() const {
-    return tsb::AxisDev{d_ws, d_tid, d_tiles, K, nb, tile_bytes, ntiles};
+    return tsb::AxisDev{d_ws, d_tid, d_tab, d_tiles, K, nb, tile_bytes, ntiles};
   }
 };
 

@@ -13,17 +13,18 @@
 //  warp 0      TMA producer: the input halo tile (R1 rows x 128 cols bf16,
 //              128B-swizzled, 4 boxes) into an nst-deep ring; B tiles are
 //              either CTA-resident (copied once) or staged per tile.
-//  warp 1      MMA issuer (one thread), software-pipelined: MMA1(t+1) is
-//              issued before MMA2(t) so the vertical pass of the next tile
-//              overlaps the V-operand epilogue of the current one.
-//                pass 1 (vertical): per 16-output-row block k
-//                  D_V[c, 16k..] = Σ_r X[r, c] · R_kᵀ[r, ·]   M=128 cols, N=16
-//                  A = staged tile (MN-major SW128), B = R tile (K-major)
-//                pass 2 (horizontal): per 16-output-column block j
-//                  D_H[i, 16j..] = Σ_c V[i, c] · C_jᵀ[c, ·]   M=128 rows, N=16
-//                  A = V (bf16 MN-major SW128, written by warps 2-5)
+//  warp 1      pass-1 MMA issuer (vertical), per 16-output-row block k:
+//                D_V[c, 16k..] = Σ_r X[r, c] · R_kᵀ[r, ·]   M=128 cols, N=16
+//                A = staged tile (MN-major SW128), B = R tile (K-major)
+//  warp 10     pass-2 MMA issuer (horizontal), per 16-output-column block j:
+//                D_H[i, 16j..] = Σ_c V[i, c] · C_jᵀ[c, ·]   M=128 rows, N=16
+//                A = V (bf16 MN-major SW128, written by warps 2-5)
 //  warps 2-5   epilogue 1: D_V (TMEM) -> bf16 -> V operand (smem, x nmid)
 //  warps 6-9   epilogue 2: D_H (TMEM) -> cast -> smem -> TMA store
+//
+// The issuing warps run converged and elect one lane per tcgen05 op; the
+// per-block window starts / tile ids are read from the kernel-parameter
+// (constant) bank so they land directly in uniform registers.
 //
 // TMEM (512 cols): D_V double-buffered at [0,128) and [128,256), D_H at
 // [256, 256 + nb2·16).  Window starts are multiples of 8 rows/cols (the
@@ -38,10 +39,11 @@
 namespace tsb {
 
 constexpr int kMaxStages = 4;
-constexpr int kThreads = 320;
+constexpr int kThreads = 352;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kMidBytes = 128 * 128 * 2;  // V tile: 128 rows x 128 cols bf16
 constexpr uint32_t kSmemLimit = 232448;        // max dynamic smem per CTA on sm_100
+constexpr int kParamTab = 3072;                // packed block entries carried in params
 
 // Shared-memory plan, chosen on the host and passed to the kernel.
 struct SepSmem {
@@ -60,8 +62,20 @@ struct SepParams {
   int nb2;    // column blocks per tile
   int R1;     // staged input rows per tile (multiple of 16)
   int nrt, nct, planes, ntiles;
+  int ptab;      // 1: block tables below, 0: read r.tab / c.tab from global
+  int ptab_c;    // offset of the cols table inside tab[]
   SepSmem L;
+  int32_t tab[kParamTab];  // packed (ws << 16) | tid, rows then cols
 };
+
+__device__ __forceinline__ int32_t tab_r(const SepParams& P, int b) {
+  return P.ptab ? P.tab[b] : P.r.tab[b];
+}
+__device__ __forceinline__ int32_t tab_c(const SepParams& P, int b) {
+  return P.ptab ? P.tab[P.ptab_c + b] : P.c.tab[b];
+}
+__device__ __forceinline__ int tab_ws(int32_t e) { return e >> 16; }
+__device__ __forceinline__ int tab_tid(int32_t e) { return e & 0xFFFF; }
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -85,23 +99,39 @@ __device__ __forceinline__ void store_out_row<float>(uint32_t dst, const uint32_
     st_shared_v4(dst + 16 * i, r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
 }
 
-struct TileCoord {
-  int p, rt, ct;
+// Persistent tile walk t = blockIdx.x + it·gridDim.x with (p, rt, ct) kept
+// incrementally (one division at start, none per tile).
+struct TileWalk {
+  int t, ct, rt, p;
+  int dct, drt;
+  __device__ __forceinline__ explicit TileWalk(const SepParams& P) {
+    t = blockIdx.x;
+    ct = t % P.nct;
+    rt = (t / P.nct) % P.nrt;
+    p = t / (P.nct * P.nrt);
+    dct = gridDim.x % P.nct;
+    drt = gridDim.x / P.nct;
+  }
+  __device__ __forceinline__ void next(const SepParams& P) {
+    t += gridDim.x;
+    ct += dct;
+    int carry = 0;
+    if (ct >= P.nct) {
+      ct -= P.nct;
+      carry = 1;
+    }
+    rt += drt + carry;
+    while (rt >= P.nrt) {
+      rt -= P.nrt;
+      ++p;
+    }
+  }
 };
-
-__device__ __forceinline__ TileCoord decode_tile(const SepParams& P, int t) {
-  TileCoord c;
-  c.ct = t % P.nct;
-  const int rest = t / P.nct;
-  c.rt = rest % P.nrt;
-  c.p = rest / P.nrt;
-  return c;
-}
 
 template <typename OutT, int KQ1, int KQ2>
 __global__ void __launch_bounds__(kThreads, 1)
     separable_kernel(const __grid_constant__ CUtensorMap tm_in,
-                     const __grid_constant__ CUtensorMap tm_out, const SepParams P) {
+                     const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ SepParams P) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_s = smem_u32(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
@@ -150,6 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nb2 = P.nb2;
   const int nst = static_cast<int>(L.nst);
   const int nmid = static_cast<int>(L.nmid);
+  const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, /*a MN-major*/ 1, /*b K-major*/ 0);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -162,152 +193,139 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_g2s(base + L.off_w + L.w1_bytes, P.c.tiles, cb, wres);
       }
       const int hr = P.R1 / 2;
-      int it = 0;
-      for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x, ++it) {
+      TileWalk tw(P);
+      for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
         const int s = it % nst;
         const uint32_t ph = (it / nst) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        const TileCoord tc = decode_tile(P, t);
-        const int b1 = tc.rt * kRowBlocksPerTile, b2 = tc.ct * nb2;
-        const int row0 = P.r.ws[b1], col0 = P.c.ws[b2];
+        const int b1 = tw.rt * kRowBlocksPerTile, b2 = tw.ct * nb2;
+        const int row0 = tab_ws(tab_r(P, b1)), col0 = tab_ws(tab_c(P, b2));
         uint32_t wbytes = 0;
         if (!L.resident) {
           for (int k = 0; k < kRowBlocksPerTile; ++k)
-            if (k == 0 || P.r.tid[b1 + k] != P.r.tid[b1 + k - 1]) wbytes += P.r.tile_bytes;
+            if (k == 0 || tab_tid(tab_r(P, b1 + k)) != tab_tid(tab_r(P, b1 + k - 1)))
+              wbytes += P.r.tile_bytes;
           for (int j = 0; j < nb2; ++j)
-            if (j == 0 || P.c.tid[b2 + j] != P.c.tid[b2 + j - 1]) wbytes += P.c.tile_bytes;
+            if (j == 0 || tab_tid(tab_c(P, b2 + j)) != tab_tid(tab_c(P, b2 + j - 1)))
+              wbytes += P.c.tile_bytes;
         }
+        mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], L.in_stage + wbytes);
         uint8_t* dst = base + s * L.in_stage;
-        tma_load_3d(dst, &tm_in, &full[s], col0, row0, tc.p);
-        tma_load_3d(dst + hr * 128, &tm_in, &full[s], col0, row0 + hr, tc.p);
-        tma_load_3d(dst + P.R1 * 128, &tm_in, &full[s], col0 + 64, row0, tc.p);
-        tma_load_3d(dst + P.R1 * 128 + hr * 128, &tm_in, &full[s], col0 + 64, row0 + hr, tc.p);
+        tma_load_3d(dst, &tm_in, &full[s], col0, row0, tw.p);
+        tma_load_3d(dst + hr * 128, &tm_in, &full[s], col0, row0 + hr, tw.p);
+        tma_load_3d(dst + P.R1 * 128, &tm_in, &full[s], col0 + 64, row0, tw.p);
+        tma_load_3d(dst + P.R1 * 128 + hr * 128, &tm_in, &full[s], col0 + 64, row0 + hr, tw.p);
         if (!L.resident) {
           uint8_t* wd = base + L.off_w + s * L.w_stage;
-          for (int k = 0; k < kRowBlocksPerTile; ++k)
-            if (k == 0 || P.r.tid[b1 + k] != P.r.tid[b1 + k - 1])
+          for (int k = 0; k < kRowBlocksPerTile; ++k) {
+            const int tid = tab_tid(tab_r(P, b1 + k));
+            if (k == 0 || tid != tab_tid(tab_r(P, b1 + k - 1)))
               bulk_g2s(wd + k * P.r.tile_bytes,
-                       P.r.tiles + static_cast<size_t>(P.r.tid[b1 + k]) * P.r.tile_bytes,
-                       P.r.tile_bytes, &full[s]);
-          for (int j = 0; j < nb2; ++j)
-            if (j == 0 || P.c.tid[b2 + j] != P.c.tid[b2 + j - 1])
+                       P.r.tiles + static_cast<size_t>(tid) * P.r.tile_bytes, P.r.tile_bytes,
+                       &full[s]);
+          }
+          for (int j = 0; j < nb2; ++j) {
+            const int tid = tab_tid(tab_c(P, b2 + j));
+            if (j == 0 || tid != tab_tid(tab_c(P, b2 + j - 1)))
               bulk_g2s(wd + L.w1_bytes + j * P.c.tile_bytes,
-                       P.c.tiles + static_cast<size_t>(P.c.tid[b2 + j]) * P.c.tile_bytes,
-                       P.c.tile_bytes, &full[s]);
+                       P.c.tiles + static_cast<size_t>(tid) * P.c.tile_bytes, P.c.tile_bytes,
+                       &full[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    // The whole warp runs this loop (converged); one elected lane issues each
-    // tcgen05 op.  Block tables are fetched lane-parallel (lane k <-> block k)
-    // before the waits so their latency hides behind the pipeline.
-    const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, /*a MN-major*/ 1, /*b K-major*/ 0);
+    // ------------------------------------------------------------ pass-1 issuer
     const uint32_t lbo_in = static_cast<uint32_t>(P.R1) * 128u;  // 64-col half stride
     const int kq1 = KQ1 > 0 ? KQ1 : P.r.K / 16;
-    const int kq2 = KQ2 > 0 ? KQ2 : P.c.K / 16;
-    const uint32_t tb1 = P.r.tile_bytes, tb2 = P.c.tile_bytes;
-    const uint32_t sbo1 = static_cast<uint32_t>(P.r.K) * 16u, sbo2 = static_cast<uint32_t>(P.c.K) * 16u;
+    const uint32_t tb1 = P.r.tile_bytes;
+    const uint32_t sbo1 = static_cast<uint32_t>(P.r.K) * 16u;
     if (L.resident) mbar_wait(wres, 0);
-    for (int it = 0;; ++it) {
-      const int t = blockIdx.x + it * gridDim.x;
-      const bool has = t < P.ntiles;
-      if (has) {
-        // ---- pass 1 of tile `it`
-        const int s = it % nst;
-        const int d = it & 1;
-        const TileCoord tc = decode_tile(P, t);
-        const int b1 = tc.rt * kRowBlocksPerTile;
-        int my_ws = 0, my_tid = 0;
-        if (lane < kRowBlocksPerTile) {
-          my_ws = P.r.ws[b1 + lane];
-          my_tid = P.r.tid[b1 + lane];
-        }
-        const int row0 = __shfl_sync(0xffffffffu, my_ws, 0);
-        const uint32_t a0 = base_s + s * L.in_stage;
-        const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
-        mbar_wait(&full[s], (it / nst) & 1);
-        mbar_wait(&dv_free[d], ((it >> 1) & 1) ^ 1);
-        __syncwarp();
-        tc_fence_after();
-        int slot = 0, prev = -1;
+    TileWalk tw(P);
+    for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
+      const int s = it % nst;
+      const int d = it & 1;
+      const int b1 = tw.rt * kRowBlocksPerTile;
+      const int row0 = tab_ws(tab_r(P, b1));
+      const uint32_t a0 = base_s + s * L.in_stage;
+      const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
+      mbar_wait(&full[s], (it / nst) & 1);
+      mbar_wait(&dv_free[d], ((it >> 1) & 1) ^ 1);
+      __syncwarp();
+      tc_fence_after();
+      int slot = 0, prev = -1;
 #pragma unroll
-        for (int k = 0; k < kRowBlocksPerTile; ++k) {
-          const int wsk = __shfl_sync(0xffffffffu, my_ws, k);
-          const int tidk = __shfl_sync(0xffffffffu, my_tid, k);
-          if (L.resident)
-            slot = tidk;
-          else if (tidk != prev)
-            slot = k;
-          prev = tidk;
-          const uint64_t ad = make_sdesc(a0 + static_cast<uint32_t>(wsk - row0) * 128u, lbo_in,
-                                         1024u, kSwizzle128B);
-          const uint64_t bd = make_sdesc(w0 + slot * tb1, 128u, sbo1, kSwizzleNone);
-          const uint32_t dcol = tmem + d * 128u + 16u * k;
+      for (int k = 0; k < kRowBlocksPerTile; ++k) {
+        const int32_t e = tab_r(P, b1 + k);
+        const int tid = tab_tid(e);
+        if (L.resident)
+          slot = tid;
+        else if (tid != prev)
+          slot = k;
+        prev = tid;
+        const uint64_t ad = make_sdesc(a0 + static_cast<uint32_t>(tab_ws(e) - row0) * 128u, lbo_in,
+                                       1024u, kSwizzle128B);
+        const uint64_t bd = make_sdesc(w0 + slot * tb1, 128u, sbo1, kSwizzleNone);
+        const uint32_t dcol = tmem + d * 128u + 16u * k;
 #pragma unroll
-          for (int q = 0; q < (KQ1 > 0 ? KQ1 : 16); ++q) {
-            if (KQ1 == 0 && q >= kq1) break;
-            // +2048 B (16 rows of A) and +256 B (two k-chunks of B) per K step
-            mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc, q > 0 ? 1u : 0u);
-          }
+        for (int q = 0; q < (KQ1 > 0 ? KQ1 : 16); ++q) {
+          if (KQ1 == 0 && q >= kq1) break;
+          // +2048 B (16 rows of A) and +256 B (two k-chunks of B) per K step
+          mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc, q > 0 ? 1u : 0u);
         }
-        mma_commit_elect(&dv_full[d]);
-        if (L.resident) mma_commit_elect(&empty[s]);
       }
-      if (it >= 1) {
-        // ---- pass 2 of tile `it - 1`
-        const int ip = it - 1;
-        const int tp = blockIdx.x + ip * gridDim.x;
-        const int s = ip % nst;
-        const int m = ip % nmid;
-        const TileCoord tc = decode_tile(P, tp);
-        const int b2 = tc.ct * nb2;
-        int my_ws = 0, my_tid = 0;
-        if (lane < nb2) {
-          my_ws = P.c.ws[b2 + lane];
-          my_tid = P.c.tid[b2 + lane];
-        }
-        const int col0 = __shfl_sync(0xffffffffu, my_ws, 0);
-        const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
-        const uint32_t mid_s = base_s + L.off_mid + m * kMidBytes;
-        mbar_wait(&mid_full[m], (ip / nmid) & 1);
-        mbar_wait(dh_free, (ip & 1) ^ 1);
-        __syncwarp();
-        tc_fence_after();
-        int slot = 0, prev = -1;
+      mma_commit_elect(&dv_full[d]);
+      if (L.resident) mma_commit_elect(&empty[s]);
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ pass-2 issuer
+    const int kq2 = KQ2 > 0 ? KQ2 : P.c.K / 16;
+    const uint32_t tb2 = P.c.tile_bytes;
+    const uint32_t sbo2 = static_cast<uint32_t>(P.c.K) * 16u;
+    if (L.resident) mbar_wait(wres, 0);
+    TileWalk tw(P);
+    for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
+      const int s = it % nst;
+      const int m = it % nmid;
+      const int b2 = tw.ct * nb2;
+      const int col0 = tab_ws(tab_c(P, b2));
+      const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
+      const uint32_t mid_s = base_s + L.off_mid + m * kMidBytes;
+      mbar_wait(&mid_full[m], (it / nmid) & 1);
+      mbar_wait(dh_free, (it & 1) ^ 1);
+      __syncwarp();
+      tc_fence_after();
+      int slot = 0, prev = -1;
 #pragma unroll 1
-        for (int j = 0; j < nb2; ++j) {
-          const int wsj = __shfl_sync(0xffffffffu, my_ws, j);
-          const int tidj = __shfl_sync(0xffffffffu, my_tid, j);
-          if (L.resident)
-            slot = tidj;
-          else if (tidj != prev)
-            slot = j;
-          prev = tidj;
-          const uint64_t ad = make_sdesc(mid_s + static_cast<uint32_t>((wsj - col0) / 8) * 1024u,
-                                         16384u, 1024u, kSwizzle128B);
-          const uint64_t bd = make_sdesc(w0 + L.w1_bytes + slot * tb2, 128u, sbo2, kSwizzleNone);
-          const uint32_t dcol = tmem + 256u + 16u * j;
+      for (int j = 0; j < nb2; ++j) {
+        const int32_t e = tab_c(P, b2 + j);
+        const int tid = tab_tid(e);
+        if (L.resident)
+          slot = tid;
+        else if (tid != prev)
+          slot = j;
+        prev = tid;
+        const uint64_t ad = make_sdesc(mid_s + static_cast<uint32_t>((tab_ws(e) - col0) / 8) * 1024u,
+                                       16384u, 1024u, kSwizzle128B);
+        const uint64_t bd = make_sdesc(w0 + L.w1_bytes + slot * tb2, 128u, sbo2, kSwizzleNone);
+        const uint32_t dcol = tmem + 256u + 16u * j;
 #pragma unroll
-          for (int q = 0; q < (KQ2 > 0 ? KQ2 : 16); ++q) {
-            if (KQ2 == 0 && q >= kq2) break;
-            mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc, q > 0 ? 1u : 0u);
-          }
+        for (int q = 0; q < (KQ2 > 0 ? KQ2 : 16); ++q) {
+          if (KQ2 == 0 && q >= kq2) break;
+          mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc, q > 0 ? 1u : 0u);
         }
-        mma_commit_elect(dh_full);
-        mma_commit_elect(&mid_free[m]);
-        if (!L.resident) mma_commit_elect(&empty[s]);
       }
-      if (!has) break;
+      mma_commit_elect(dh_full);
+      mma_commit_elect(&mid_free[m]);
+      if (!L.resident) mma_commit_elect(&empty[s]);
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue 1
     const int quarter = warp & 3;       // TMEM lane quarter this warp may access
     const int c = quarter * 32 + lane;  // input column within the tile
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    int it = 0;
-    for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x, ++it) {
+    TileWalk tw(P);
+    for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
       const int d = it & 1;
       const int m = it % nmid;
       const uint32_t mid_row =
@@ -350,9 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + 256u;
     const uint32_t out_row_bytes = static_cast<uint32_t>(nb2 * 16 * sizeof(OutT));
     const uint32_t orow = base_s + L.off_out + row * out_row_bytes;
-    int it = 0;
-    for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x, ++it) {
-      const TileCoord tc = decode_tile(P, t);
+    TileWalk tw(P);
+    for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
       mbar_wait(dh_full, it & 1);
       tc_fence_after();
       uint32_t r[8][16];
@@ -370,8 +387,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       named_bar_sync(2, 128);
       if (et == 0) {
-        tma_store_3d(&tm_out, base + L.off_out, tc.ct * nb2 * 16, tc.rt * kRowBlocksPerTile * 16,
-                     tc.p);
+        tma_store_3d(&tm_out, base + L.off_out, tw.ct * nb2 * 16, tw.rt * kRowBlocksPerTile * 16,
+                     tw.p);
         bulk_commit();
       }
     }
@@ -528,6 +545,13 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
   P.nct = (ca->nb + P.nb2 - 1) / P.nb2;
   P.planes = planes;
   P.ntiles = planes * P.nrt * P.nct;
+  const int ntr = static_cast<int>(ra->tab.size()), ntc = static_cast<int>(ca->tab.size());
+  P.ptab = (ntr + ntc <= kParamTab) ? 1 : 0;
+  P.ptab_c = ntr;
+  if (P.ptab) {
+    for (int i = 0; i < ntr; ++i) P.tab[i] = ra->tab[i];
+    for (int i = 0; i < ntc; ++i) P.tab[ntr + i] = ca->tab[i];
+  }
   if (!plan_smem(P, oes))
     return set_error(TS_ERR_UNSUPPORTED, "separable: tile (R1=%d, nb2=%d) does not fit smem",
                      P.R1, P.nb2);
