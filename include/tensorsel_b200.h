@@ -134,6 +134,13 @@ TS_API ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* s
  * f32, p*l entries) into out (device f32).  Replaces the Python double loop. */
 TS_API ts_status ts_matrix_for(int l, int k, int s, int p, const float* kernel, float* out, void* stream);
 
+/* Diagnostics: make subsequent ts_separable_run launches record clock64()
+ * stamps for the first `tiles` tiles of CTAs [0, ctas) into device_buffer
+ * (u64[ctas][tiles][10]; events: 0 producer ready, 1 stage free, 2 input
+ * landed, 3 pass-1 issued, 4 D_V ready, 5 V operand written, 6 pass-2 start,
+ * 7 pass-2 issued, 8 D_H ready, 9 output stored).  NULL turns it off. */
+TS_API ts_status ts_debug_trace(void* device_buffer, int ctas, int tiles);
+
 /* Diagnostics: one tcgen05 MMA  D(128 x n) = A(128 x k) · B(k x n)  with A
  * staged MN-major 128B-swizzled and B K-major interleaved exactly as the
  * separable kernel stages them.  a: row-major f32 (128 x k), b: row-major

@@ -55,6 +55,7 @@ _SIGNATURES = {
     "ts_cast_f32_bf16": (_I, [_P, _P, _I64, _P]),
     "ts_matrix_for": (_I, [_I, _I, _I, _I, _P, _P, _P]),
     "ts_probe_umma": (_I, [_P, _P, _P, _I, _I, _P]),
+    "ts_debug_trace": (_I, [_P, _I, _I]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

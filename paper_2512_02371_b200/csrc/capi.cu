@@ -15,6 +15,7 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
                         int64_t out_ps, int out_dtype, cudaStream_t stream);
 ts_status separable_plan(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype,
                          int* out8);
+void set_trace(void* buf, int ctas, int tiles);
 
 // ------------------------------------------------------------------ cast
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -158,6 +159,13 @@ ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int planes,
 ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes, int out_dtype,
                             int* out8) {
   return separable_plan(rows, cols, planes, out_dtype, out8);
+}
+
+ts_status ts_debug_trace(void* device_buffer, int ctas, int tiles) {
+  if (device_buffer && (ctas < 1 || tiles < 1))
+    return set_error(TS_ERR_INVALID, "trace: ctas and tiles must be >= 1");
+  set_trace(device_buffer, ctas, tiles);
+  return TS_OK;
 }
 
 ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream) {

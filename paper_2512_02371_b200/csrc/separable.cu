@@ -62,6 +62,8 @@ struct SepParams {
   int nb2;    // column blocks per tile
   int R1;     // staged input rows per tile (multiple of 16)
   int nrt, nct, planes, ntiles;
+  unsigned long long* trace;  // diagnostics: per-(CTA, tile, event) clock64 stamps or null
+  int trace_ctas, trace_tiles;
   int ptab;      // 1: block tables below, 0: read r.tab / c.tab from global
   int ptab_c;    // offset of the cols table inside tab[]
   SepSmem L;
@@ -75,6 +77,13 @@ __device__ __forceinline__ int32_t tab_c(const SepParams& P, int b) {
   return P.ptab ? P.tab[P.ptab_c + b] : P.c.tab[b];
 }
 __device__ __forceinline__ int tab_ws(int32_t e) { return e >> 16; }
+
+// Diagnostics: stamp event `ev` of tile `it` (events 0..9, see ts_debug_trace).
+__device__ __forceinline__ void trace_stamp(const SepParams& P, int it, int ev) {
+  if (P.trace != nullptr && static_cast<int>(blockIdx.x) < P.trace_ctas && it < P.trace_tiles &&
+      (threadIdx.x & 31) == 0)
+    P.trace[(static_cast<size_t>(blockIdx.x) * P.trace_tiles + it) * 10 + ev] = clock64();
+}
 __device__ __forceinline__ int tab_tid(int32_t e) { return e & 0xFFFF; }
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
@@ -208,7 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j == 0 || tab_tid(tab_c(P, b2 + j)) != tab_tid(tab_c(P, b2 + j - 1)))
               wbytes += P.c.tile_bytes;
         }
+        trace_stamp(P, it, 0);
         mbar_wait(&empty[s], ph ^ 1);
+        trace_stamp(P, it, 1);
         mbar_arrive_expect_tx(&full[s], L.in_stage + wbytes);
         uint8_t* dst = base + s * L.in_stage;
         tma_load_3d(dst, &tm_in, &full[s], col0, row0, tw.p);
@@ -250,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t a0 = base_s + s * L.in_stage;
       const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
       mbar_wait(&full[s], (it / nst) & 1);
+      trace_stamp(P, it, 2);
       mbar_wait(&dv_free[d], ((it >> 1) & 1) ^ 1);
       __syncwarp();
       tc_fence_after();
@@ -276,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_commit_elect(&dv_full[d]);
       if (L.resident) mma_commit_elect(&empty[s]);
+      trace_stamp(P, it, 3);
     }
   } else if (warp == 10) {
     // ------------------------------------------------------------ pass-2 issuer
@@ -292,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
       const uint32_t mid_s = base_s + L.off_mid + m * kMidBytes;
       mbar_wait(&mid_full[m], (it / nmid) & 1);
+      trace_stamp(P, it, 6);
       mbar_wait(dh_free, (it & 1) ^ 1);
       __syncwarp();
       tc_fence_after();
@@ -318,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit_elect(dh_full);
       mma_commit_elect(&mid_free[m]);
       if (!L.resident) mma_commit_elect(&empty[s]);
+      trace_stamp(P, it, 7);
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue 1
@@ -331,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t mid_row =
           base_s + L.off_mid + m * kMidBytes + (c / 8) * 1024u + (c % 8) * 128u;
       mbar_wait(&dv_full[d], (it >> 1) & 1);
+      if (warp == 2) trace_stamp(P, it, 4);
       mbar_wait(&mid_free[m], ((it / nmid) & 1) ^ 1);
       tc_fence_after();
 #pragma unroll
@@ -359,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       fence_proxy_async_smem();
       mbar_arrive(&mid_full[m]);
+      if (warp == 2) trace_stamp(P, it, 5);
     }
   } else {
     // ------------------------------------------------------------ epilogue 2
@@ -371,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     TileWalk tw(P);
     for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
       mbar_wait(dh_full, it & 1);
+      if (warp == 6) trace_stamp(P, it, 8);
       tc_fence_after();
       uint32_t r[8][16];
 #pragma unroll
@@ -391,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      tw.p);
         bulk_commit();
       }
+      if (warp == 6) trace_stamp(P, it, 9);
     }
     if (et == 0) bulk_wait0();
   }
@@ -529,8 +548,20 @@ static ts_status launch_sep(const SepParams& P, const CUtensorMap& tin, const CU
   }
 }
 
+static unsigned long long* g_trace = nullptr;
+static int g_trace_ctas = 0, g_trace_tiles = 0;
+
+void set_trace(void* buf, int ctas, int tiles) {
+  g_trace = static_cast<unsigned long long*>(buf);
+  g_trace_ctas = buf ? ctas : 0;
+  g_trace_tiles = buf ? tiles : 0;
+}
+
 static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, int oes,
                              SepParams& P) {
+  P.trace = g_trace;
+  P.trace_ctas = g_trace_ctas;
+  P.trace_tiles = g_trace_tiles;
   if (ra->row_span > kMaxRowSpan || ra->row_span % 16)
     return set_error(TS_ERR_UNSUPPORTED, "rows axis: row tile span %d > %d", ra->row_span,
                      kMaxRowSpan);
