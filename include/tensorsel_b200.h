@@ -148,6 +148,15 @@ TS_API ts_status ts_debug_trace(void* device_buffer, int ctas, int tiles);
  * n % 16 == 0, n <= 256, k <= 256. */
 TS_API ts_status ts_probe_umma(const float* a, const float* b, float* d, int k, int n, void* stream);
 
+/* Diagnostics: tcgen05 operand-mode probe.  D(128 x n) = A(128 x k) · B(k x n),
+ * the K loop issued `reps` times into one accumulator; *cycles (device
+ * pointer, may be NULL) receives clock64 cycles from first issue to
+ * completion.  amode 0: A smem MN-major SW128 bf16, 1: A smem K-major bf16,
+ * 2: A in TMEM f32 (kind::tf32); bmode 0: B smem K-major (bf16, f32 for
+ * amode 2), 1: B smem MN-major SW128 bf16. */
+TS_API ts_status ts_probe_mma(int amode, int bmode, const float* a, const float* b, float* d,
+                              int k, int n, int reps, long long* cycles, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

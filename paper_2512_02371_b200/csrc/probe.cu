@@ -1,0 +1,185 @@
+// probe.cu — tcgen05 operand-mode probe (diagnostics, used by tests and for
+// kernel design): one CTA stages A (128 x k) and B (k x n) in a chosen
+// layout, issues the K loop `reps` times into one TMEM accumulator and
+// reports D plus the clock64 cycles from first issue to completion.
+//
+//   amode 0: A in smem, MN-major, 128B swizzle (bf16)
+//   amode 1: A in smem, K-major, no swizzle core matrices (bf16)
+//   amode 2: A in TMEM, f32 read as tf32 (kind::tf32), lane = row, column = k
+//   bmode 0: B in smem, K-major, no swizzle (bf16; f32 for amode 2)
+//   bmode 1: B in smem, MN-major, 128B swizzle (bf16)
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "sm100.cuh"
+
+namespace tsb {
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1)
+    probe_mma_kernel(int amode, int bmode, const float* __restrict__ a, const float* __restrict__ b,
+                     float* __restrict__ d, int k, int n, int reps, long long* cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_s = smem_u32(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_s - raw_s);
+  const bool tf32 = amode == 2;
+  const int es = tf32 ? 4 : 2;
+  const uint32_t a_bytes = tf32 ? 0u : 128u * k * 2u;
+  const uint32_t b_bytes = static_cast<uint32_t>(k) * n * es;
+  uint8_t* sa = base;
+  uint8_t* sb = base + a_bytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + a_bytes + ((b_bytes + 1023u) & ~1023u));
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- stage A
+  const uint32_t lbo_a_mn = static_cast<uint32_t>(k / 8) * 1024u;  // m-atom stride (amode 0)
+  const uint32_t sbo_a_k = static_cast<uint32_t>(k / 8) * 128u;    // 8-row group stride (amode 1)
+  if (!tf32) {
+    for (int e = threadIdx.x; e < 128 * k; e += blockDim.x) {
+      const int m = e / k, kk = e % k;
+      uint32_t off;
+      if (amode == 0)
+        off = (m / 64) * lbo_a_mn + (kk / 8) * 1024u + (kk % 8) * 128u +
+              ((((m % 64) / 8) ^ (kk % 8)) * 16u) + (m % 8) * 2u;
+      else
+        off = (m / 8) * sbo_a_k + (kk / 8) * 128u + (m % 8) * 16u + (kk % 8) * 2u;
+      *reinterpret_cast<__nv_bfloat16*>(sa + off) = __float2bfloat16_rn(a[e]);
+    }
+  }
+  // ---- stage B
+  const uint32_t lbo_b_mn = static_cast<uint32_t>(k / 8) * 1024u;  // n-atom stride (bmode 1)
+  for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
+    const int kk = e / n, nn = e % n;
+    if (tf32) {
+      const uint32_t off = (nn / 8) * (static_cast<uint32_t>(k / 4) * 128u) + (kk / 4) * 128u +
+                           (nn % 8) * 16u + (kk % 4) * 4u;
+      *reinterpret_cast<float*>(sb + off) = b[e];
+    } else {
+      uint32_t off;
+      if (bmode == 0)
+        off = (nn / 8) * (k * 16u) + (kk / 8) * 128u + (nn % 8) * 16u + (kk % 8) * 2u;
+      else
+        off = (nn / 64) * lbo_b_mn + (kk / 8) * 1024u + (kk % 8) * 128u +
+              ((((nn % 64) / 8) ^ (kk % 8)) * 16u) + (nn % 8) * 2u;
+      *reinterpret_cast<__nv_bfloat16*>(sb + off) = __float2bfloat16_rn(b[e]);
+    }
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+
+  if (tf32) {
+    // A row m = this thread's TMEM lane, columns [256, 256 + k)
+    const int m = warp * 32 + lane;
+    for (int c0 = 0; c0 < k; c0 += 16) {
+      uint32_t r[16];
+      for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(a[m * k + c0 + i]);
+      tmem_st16(lane_base + 256u + c0, r);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+
+  long long t0 = 0, t1 = 0;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc =
+        make_idesc(tf32 ? kFmtTF32 : kFmtBF16, 128, n, amode == 0 ? 1u : 0u, bmode == 1 ? 1u : 0u);
+    const int kstep = tf32 ? 8 : 16;
+    t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      for (int q = 0; q < k / kstep; ++q) {
+        const uint32_t acc = (r > 0 || q > 0) ? 1u : 0u;
+        if (tf32) {
+          const uint64_t bd = make_sdesc(base_s + a_bytes + q * 256u, 128u,
+                                         static_cast<uint32_t>(k / 4) * 128u, kSwizzleNone);
+          mma_tf32_ts(tmem, tmem + 256u + q * 8u, bd, idesc, acc);
+        } else {
+          const uint64_t ad =
+              amode == 0 ? make_sdesc(base_s + q * 2048u, lbo_a_mn, 1024u, kSwizzle128B)
+                         : make_sdesc(base_s + q * 256u, 128u, sbo_a_k, kSwizzleNone);
+          const uint64_t bd =
+              bmode == 0 ? make_sdesc(base_s + a_bytes + q * 256u, 128u, k * 16u, kSwizzleNone)
+                         : make_sdesc(base_s + a_bytes + q * 2048u, lbo_b_mn, 1024u, kSwizzle128B);
+          mma_f16_ss(tmem, ad, bd, idesc, acc);
+        }
+      }
+    }
+    mma_commit(bar);
+  }
+  __syncwarp();
+  mbar_wait(bar, 0);
+  if (threadIdx.x == 0) {
+    t1 = clock64();
+    if (cycles) *cycles = t1 - t0;
+  }
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  for (int c0 = 0; c0 < n; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(lane_base + c0, r);
+    tmem_wait_ld();
+    for (int i = 0; i < 16; ++i) d[row * n + c0 + i] = __uint_as_float(r[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace tsb
+
+using namespace tsb;
+
+extern "C" ts_status ts_probe_mma(int amode, int bmode, const float* a, const float* b, float* d,
+                                  int k, int n, int reps, long long* cycles, void* stream) {
+  const int kstep = amode == 2 ? 8 : 16;
+  if (amode < 0 || amode > 2 || bmode < 0 || bmode > 1 || (amode == 2 && bmode != 0) || !a ||
+      !b || !d || k < kstep || k > 256 || k % 16 || n < 16 || n > 256 || n % 16 || reps < 1)
+    return set_error(TS_ERR_INVALID, "probe_mma: bad arguments");
+  const int es = amode == 2 ? 4 : 2;
+  const uint32_t a_bytes = amode == 2 ? 0u : 128u * k * 2u;
+  const uint32_t b_bytes = static_cast<uint32_t>(k) * n * es;
+  const uint32_t smem = 1024 + a_bytes + ((b_bytes + 1023u) & ~1023u) + 64;
+  cudaError_t e =
+      cudaFuncSetAttribute(probe_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_error(e, "probe_mma smem attribute");
+  probe_mma_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(amode, bmode, a, b, d, k,
+                                                                        n, reps, cycles);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_mma launch");
+}
