@@ -153,9 +153,16 @@ TS_API ts_status ts_probe_umma(const float* a, const float* b, float* d, int k, 
  * pointer, may be NULL) receives clock64 cycles from first issue to
  * completion.  amode 0: A smem MN-major SW128 bf16, 1: A smem K-major bf16,
  * 2: A in TMEM f32 (kind::tf32); bmode 0: B smem K-major (bf16, f32 for
- * amode 2), 1: B smem MN-major SW128 bf16. */
+ * amode 2), 1: B smem MN-major SW128 bf16.  nacc > 1 round-robins the
+ * repetitions over nacc accumulators (columns [n*i, n*i + n)) to measure
+ * independent-MMA throughput; d then holds accumulator 0. */
 TS_API ts_status ts_probe_mma(int amode, int bmode, const float* a, const float* b, float* d,
-                              int k, int n, int reps, long long* cycles, void* stream);
+                              int k, int n, int reps, long long* cycles, int nacc, void* stream);
+
+/* Diagnostics: tcgen05.mma issue-rate microbenchmark (64 warp-converged,
+ * elect-issued M=128 K=16 MMAs; variant 0..5 = N/accumulators (16,1) (16,8)
+ * (64,1) (64,4) (256,1) (256,2)); *cycles (device) = cycles to completion. */
+TS_API ts_status ts_probe_issue(int variant, long long* cycles, void* stream);
 
 #ifdef __cplusplus
 }

@@ -56,7 +56,8 @@ _SIGNATURES = {
     "ts_matrix_for": (_I, [_I, _I, _I, _I, _P, _P, _P]),
     "ts_probe_umma": (_I, [_P, _P, _P, _I, _I, _P]),
     "ts_debug_trace": (_I, [_P, _I, _I]),
-    "ts_probe_mma": (_I, [_I, _I, _P, _P, _P, _I, _I, _I, _P, _P]),
+    "ts_probe_mma": (_I, [_I, _I, _P, _P, _P, _I, _I, _I, _P, _I, _P]),
+    "ts_probe_issue": (_I, [_I, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -39,7 +39,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 
 __global__ void __launch_bounds__(128, 1)
     probe_mma_kernel(int amode, int bmode, const float* __restrict__ a, const float* __restrict__ b,
-                     float* __restrict__ d, int k, int n, int reps, long long* cycles) {
+                     float* __restrict__ d, int k, int n, int reps, long long* cycles, int nacc) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_s = smem_u32(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
@@ -120,12 +120,15 @@ __global__ void __launch_bounds__(128, 1)
     const int kstep = tf32 ? 8 : 16;
     t0 = clock64();
     for (int r = 0; r < reps; ++r) {
+      // nacc > 1: round-robin the repetitions over nacc accumulators (columns
+      // n*i .. n*i+n-1) so consecutive K loops are independent
+      const uint32_t dcol = static_cast<uint32_t>((r % nacc) * n);
       for (int q = 0; q < k / kstep; ++q) {
-        const uint32_t acc = (r > 0 || q > 0) ? 1u : 0u;
+        const uint32_t acc = (r >= nacc || q > 0) ? 1u : 0u;
         if (tf32) {
           const uint64_t bd = make_sdesc(base_s + a_bytes + q * 256u, 128u,
                                          static_cast<uint32_t>(k / 4) * 128u, kSwizzleNone);
-          mma_tf32_ts(tmem, tmem + 256u + q * 8u, bd, idesc, acc);
+          mma_tf32_ts(tmem + dcol, tmem + 256u + q * 8u, bd, idesc, acc);
         } else {
           const uint64_t ad =
               amode == 0 ? make_sdesc(base_s + q * 2048u, lbo_a_mn, 1024u, kSwizzle128B)
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(128, 1)
           const uint64_t bd =
               bmode == 0 ? make_sdesc(base_s + a_bytes + q * 256u, 128u, k * 16u, kSwizzleNone)
                          : make_sdesc(base_s + a_bytes + q * 2048u, lbo_b_mn, 1024u, kSwizzle128B);
-          mma_f16_ss(tmem, ad, bd, idesc, acc);
+          mma_f16_ss(tmem + dcol, ad, bd, idesc, acc);
         }
       }
     }
@@ -166,10 +169,12 @@ __global__ void __launch_bounds__(128, 1)
 using namespace tsb;
 
 extern "C" ts_status ts_probe_mma(int amode, int bmode, const float* a, const float* b, float* d,
-                                  int k, int n, int reps, long long* cycles, void* stream) {
+                                  int k, int n, int reps, long long* cycles, int nacc,
+                                  void* stream) {
   const int kstep = amode == 2 ? 8 : 16;
   if (amode < 0 || amode > 2 || bmode < 0 || bmode > 1 || (amode == 2 && bmode != 0) || !a ||
-      !b || !d || k < kstep || k > 256 || k % 16 || n < 16 || n > 256 || n % 16 || reps < 1)
+      !b || !d || k < kstep || k > 256 || k % 16 || n < 16 || n > 256 || n % 16 || reps < 1 ||
+      nacc < 1 || nacc * n > (amode == 2 ? 256 : 512))
     return set_error(TS_ERR_INVALID, "probe_mma: bad arguments");
   const int es = amode == 2 ? 4 : 2;
   const uint32_t a_bytes = amode == 2 ? 0u : 128u * k * 2u;
@@ -179,7 +184,78 @@ extern "C" ts_status ts_probe_mma(int amode, int bmode, const float* a, const fl
       cudaFuncSetAttribute(probe_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_error(e, "probe_mma smem attribute");
   probe_mma_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(amode, bmode, a, b, d, k,
-                                                                        n, reps, cycles);
+                                                                        n, reps, cycles, nacc);
   e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_mma launch");
+}
+
+// ---------------------------------------------------------------------------
+// Issue-rate microbenchmark: one warp (converged) issues COUNT tcgen05.mma
+// (M=128, K=16, N) with precomputed descriptors, fully unrolled, round-robin
+// over NACC accumulators; returns clock64 cycles from first issue to the
+// commit's completion.  Operands are uninitialised smem (values unused).
+namespace tsb {
+template <int N, int NACC, int COUNT, int ASRC>
+__global__ void __launch_bounds__(128, 1) probe_issue_kernel(long long* cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_s = smem_u32(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + (base_s - raw_s) + 65536);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (warp == 0) {
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, N, ASRC == 0 ? 1u : 0u, 0u);
+    const uint64_t ad = make_sdesc(base_s, 4096u, 1024u, kSwizzle128B);
+    const uint64_t bd = make_sdesc(base_s + 32768u, 128u, 256u, kSwizzleNone);
+    __syncwarp();
+    const long long t0 = clock64();
+#pragma unroll
+    for (int i = 0; i < COUNT; ++i)
+      mma_f16_ss_elect(tmem + (i % NACC) * N, ad, bd, idesc, i >= NACC ? 1u : 0u);
+    mma_commit_elect(bar);
+    mbar_wait(bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) *cycles = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int N, int NACC>
+static cudaError_t launch_issue(long long* cycles, cudaStream_t s) {
+  auto k = probe_issue_kernel<N, NACC, 64, 0>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  if (e != cudaSuccess) return e;
+  k<<<1, 128, 70000, s>>>(cycles);
+  return cudaGetLastError();
+}
+}  // namespace tsb
+
+// variant: 0..5 = (N, NACC) in {(16,1), (16,8), (64,1), (64,4), (256,1), (256,2)}
+extern "C" ts_status ts_probe_issue(int variant, long long* cycles, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  switch (variant) {
+    case 0: e = launch_issue<16, 1>(cycles, s); break;
+    case 1: e = launch_issue<16, 8>(cycles, s); break;
+    case 2: e = launch_issue<64, 1>(cycles, s); break;
+    case 3: e = launch_issue<64, 4>(cycles, s); break;
+    case 4: e = launch_issue<256, 1>(cycles, s); break;
+    case 5: e = launch_issue<256, 2>(cycles, s); break;
+    default: return set_error(TS_ERR_INVALID, "probe_issue: variant 0..5");
+  }
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_issue launch");
 }
