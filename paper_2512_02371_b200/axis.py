@@ -113,3 +113,17 @@ def convolution(n: int, kernel, device: int) -> Axis:
         first, w = filters.conv_axis(n, kernel)
         return Axis(n, n, first, w, device=device)
     return cached(("conv", n, kernel.tobytes(), device), build)
+
+
+def resample_filter(n_in: int, n_mid: int, kernel, device: int) -> Axis:
+    """Lanczos-3 resample n_in -> n_mid followed by a same-size centred
+    filter, composed into one banded axis (config 5 runs as ONE pass)."""
+    from . import partition
+    kernel = np.asarray(kernel, dtype=np.float32)
+
+    def build():
+        inner = filters.lanczos3_axis(n_in, n_mid)
+        outer = filters.conv_axis(n_mid, kernel)
+        first, w = partition.compose_axes(outer, inner, n_mid, n_in)
+        return Axis(n_in, n_mid, first, w, device=device)
+    return cached(("lanczos+conv", n_in, n_mid, kernel.tobytes(), device), build)

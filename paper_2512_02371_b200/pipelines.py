@@ -114,6 +114,19 @@ def box_blur(x, taps: int, *, out_dtype=None):
     return filter_separable(x, k, k, out_dtype=out_dtype)
 
 
+def resample_filter(x, out_h: int, out_w: int, taps: int = 9, sigma: float | None = None, *,
+                    out_dtype=None):
+    """Lanczos-3 resample to (out_h, out_w), then a `taps`-tap Gaussian at the
+    output resolution (config 5) — fused into ONE separable pass by composing
+    the two banded axes on the host (no intermediate image in HBM)."""
+    dev = _check_device(x)
+    H, W = x.shape[-2], x.shape[-1]
+    k = filters.gaussian_taps(taps, sigma)
+    ra = _axis.resample_filter(H, out_h, k, dev)
+    ca = _axis.resample_filter(W, out_w, k, dev)
+    return _run(x, ra, ca, out_dtype)
+
+
 def separable(x, rows: "_axis.Axis", cols: "_axis.Axis", *, out_dtype=None):
     """Apply explicit axes: out = rows · x · colsᵀ per plane."""
     return _run(x, rows, cols, out_dtype)

@@ -116,3 +116,15 @@ def test_linearity_at_full_size():
     torch.cuda.synchronize()
     # inputs of the lhs are re-rounded to bf16, so allow bf16-level differences
     assert (lhs - rhs).abs().max().item() <= 1e-2
+
+
+def test_resample_then_filter_fused_matches_two_pass_oracle():
+    # config 5: resample -> 9-tap Gaussian composed into one pass
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = _img((3, 432, 768), 21)
+    y = _gpu(pipelines.resample_filter, x, out_h=216, out_w=384, taps=9,
+             out_dtype=torch.float32)
+    ref = pipelines_ref.gaussian_blur(pipelines_ref.resample(x, 216, 384), 9)
+    assert y.shape == ref.shape
+    assert np.abs(y - ref).max() <= TOL
