@@ -126,6 +126,17 @@ TS_API ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int 
 TS_API ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes,
                                    int out_dtype, int* out8);
 
+/* Fused DCT-16 transform-domain denoise: 16x16 tiles at
+ * stride 8, sine window folded into the DCT-II matrices, coring of every
+ * non-DC coefficient (soft = 0: |c| < threshold -> 0; soft = 1: shrink by
+ * threshold), windowed inverse, overlap-add; clamp-to-edge outside the
+ * image.  in: bf16 planes (height x width, both multiples of 8); out: bf16
+ * or f32.  One sm_100a kernel (tcgen05, TMEM-resident coefficients). */
+TS_API ts_status ts_denoise_dct16(const void* in, int64_t in_row_stride, int64_t in_plane_stride,
+                                  int in_dtype, void* out, int64_t out_row_stride,
+                                  int64_t out_plane_stride, int out_dtype, int planes, int height,
+                                  int width, float threshold, int soft, void* stream);
+
 /* Elementwise f32 -> bf16 (round to nearest even), n elements. */
 TS_API ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream);
 
@@ -163,6 +174,9 @@ TS_API ts_status ts_probe_mma(int amode, int bmode, const float* a, const float*
  * elect-issued M=128 K=16 MMAs; variant 0..5 = N/accumulators (16,1) (16,8)
  * (64,1) (64,4) (256,1) (256,2)); *cycles (device) = cycles to completion. */
 TS_API ts_status ts_probe_issue(int variant, long long* cycles, void* stream);
+/* Same with A read from TMEM (TS mode); variant 0..3 = (N, kind) in
+ * {(16, f16), (64, f16), (16, tf32), (64, tf32)}. */
+TS_API ts_status ts_probe_issue_ts(int variant, long long* cycles, void* stream);
 
 #ifdef __cplusplus
 }

@@ -259,3 +259,84 @@ extern "C" ts_status ts_probe_issue(int variant, long long* cycles, void* stream
   }
   return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_issue launch");
 }
+
+// TS-mode issue rate: A from TMEM (kind::tf32 or kind::f16), B in smem.
+namespace tsb {
+__device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t acc, bool tf32) {
+  if (tf32)
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+template <int N, int TF32>
+__global__ void __launch_bounds__(128, 1) probe_issue_ts_kernel(long long* cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_s = smem_u32(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + (base_s - raw_s) + 32768);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (warp == 0) {
+    const uint32_t idesc = make_idesc(TF32 ? kFmtTF32 : kFmtBF16, 128, N, 0u, 0u);
+    const uint64_t bd = make_sdesc(base_s, 128u, 256u, kSwizzleNone);
+    __syncwarp();
+    const long long t0 = clock64();
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      mma_ts_elect(tmem + (i % 4) * N, tmem + 256u + (i % 8) * 8u, bd, idesc, i >= 4 ? 1u : 0u,
+                   TF32 != 0);
+    mma_commit_elect(bar);
+    mbar_wait(bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) *cycles = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int N, int TF32>
+static cudaError_t launch_issue_ts(long long* cycles, cudaStream_t s) {
+  auto k = probe_issue_ts_kernel<N, TF32>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
+  if (e != cudaSuccess) return e;
+  k<<<1, 128, 40000, s>>>(cycles);
+  return cudaGetLastError();
+}
+}  // namespace tsb
+
+// variant: 0..3 = (N, kind) in {(16, f16), (64, f16), (16, tf32), (64, tf32)}
+extern "C" ts_status ts_probe_issue_ts(int variant, long long* cycles, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  switch (variant) {
+    case 0: e = launch_issue_ts<16, 0>(cycles, s); break;
+    case 1: e = launch_issue_ts<64, 0>(cycles, s); break;
+    case 2: e = launch_issue_ts<16, 1>(cycles, s); break;
+    case 3: e = launch_issue_ts<64, 1>(cycles, s); break;
+    default: return set_error(TS_ERR_INVALID, "probe_issue_ts: variant 0..3");
+  }
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_issue_ts launch");
+}

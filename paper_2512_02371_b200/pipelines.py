@@ -127,6 +127,34 @@ def resample_filter(x, out_h: int, out_w: int, taps: int = 9, sigma: float | Non
     return _run(x, ra, ca, out_dtype)
 
 
+def denoise_dct16(x, threshold: float = 0.15, mode: str = "hard", *, out_dtype=None):
+    """DCT-16 transform-domain coring (config 4): 16x16
+    tiles at stride 8, sine-windowed DCT-II, coefficients below `threshold`
+    zeroed (mode="hard", the paper's coring) or shrunk (mode="soft"), DC
+    kept, windowed inverse + overlap-add, clamp-to-edge.  One fused kernel.
+    Height and width must be multiples of 8."""
+    torch = _torch()
+    _check_device(x)
+    if mode not in ("hard", "soft"):
+        raise ValueError("mode must be 'hard' or 'soft'")
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    H, W = x.shape[-2], x.shape[-1]
+    out_dtype = out_dtype or (x.dtype if x.dtype in (torch.bfloat16, torch.float32)
+                              else torch.bfloat16)
+    inb, in_rs = _as_planes_bf16(x, stream)
+    P = inb.shape[0]
+    align = 8 if out_dtype == torch.bfloat16 else 4
+    owp = -(-W // align) * align
+    out = torch.empty((P, H, owp), dtype=out_dtype, device=x.device)
+    _lib.check(_lib.load().ts_denoise_dct16(
+        inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16, out.data_ptr(), owp, owp * H,
+        _lib.TS_BF16 if out_dtype == torch.bfloat16 else _lib.TS_F32, P, H, W,
+        float(threshold), 1 if mode == "soft" else 0, stream), "ts_denoise_dct16")
+    if owp != W:
+        out = out[:, :, :W]
+    return out.reshape(*x.shape[:-2], H, W)
+
+
 def separable(x, rows: "_axis.Axis", cols: "_axis.Axis", *, out_dtype=None):
     """Apply explicit axes: out = rows · x · colsᵀ per plane."""
     return _run(x, rows, cols, out_dtype)

@@ -7,3 +7,8 @@ for v in range(6):
     for rep in range(3):
         _lib.check(L.ts_probe_issue(v, c.data_ptr(), None)); torch.cuda.synchronize()
     print(json.dumps({"variant": names[v], "cycles_64_mma": c.item(), "cyc_per_mma": c.item() / 64}))
+names = ["TS N16 f16", "TS N64 f16", "TS N16 tf32", "TS N64 tf32"]
+for v in range(4):
+    for rep in range(3):
+        _lib.check(L.ts_probe_issue_ts(v, c.data_ptr(), None)); torch.cuda.synchronize()
+    print(json.dumps({"variant": names[v], "cycles_64_mma": c.item(), "cyc_per_mma": c.item() / 64}))

@@ -1,0 +1,68 @@
+"""DCT-16 denoise (config 4) against the CPU oracle.
+
+Soft coring is Lipschitz, so the north-star bound applies directly
+(max |gpu - oracle| <= 1e-2).  Hard coring (the paper's) is discontinuous:
+a coefficient within rounding distance of the threshold can be kept by one
+side and zeroed by the other, so for it the bound is checked on all but a
+tiny fraction of pixels, and the flips are bounded in size.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import pipelines_ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _noisy(shape, seed):
+    rng = np.random.default_rng(seed)
+    H, W = shape[-2:]
+    yy, xx = np.mgrid[0:H, 0:W]
+    clean = 0.5 + 0.4 * np.sin(xx / 17.0) * np.cos(yy / 23.0)
+    x = np.clip(clean + rng.normal(0, 0.05, shape), 0, 1).astype(np.float32)
+    import torch
+    return torch.from_numpy(x).bfloat16().float().numpy()
+
+
+def _gpu(x, **kw):
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    y = pipelines.denoise_dct16(torch.from_numpy(x).bfloat16().cuda(), out_dtype=torch.float32, **kw)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+@pytest.mark.parametrize("shape", [(1, 16, 16), (1, 24, 40), (2, 136, 248), (3, 224, 224)])
+def test_threshold_zero_reconstructs_input(shape):
+    x = _noisy(shape, 1)
+    y = _gpu(x, threshold=0.0, mode="soft")
+    assert y.shape == x.shape
+    assert np.abs(y - x).max() <= 1e-2
+
+
+@pytest.mark.parametrize("shape", [(1, 64, 96), (3, 232, 360), (1, 1080, 1920)])
+def test_soft_coring_matches_oracle(shape):
+    x = _noisy(shape, 2)
+    y = _gpu(x, threshold=0.15, mode="soft")
+    ref = pipelines_ref.dct_denoise(x, 0.15, "soft")
+    assert np.abs(y - ref).max() <= 1e-2
+
+
+@pytest.mark.parametrize("shape", [(1, 232, 360), (1, 2160, 3840)])
+def test_hard_coring_matches_oracle_up_to_threshold_flips(shape):
+    x = _noisy(shape, 3)
+    y = _gpu(x, threshold=0.15, mode="hard")
+    ref = pipelines_ref.dct_denoise(x, 0.15, "hard")
+    d = np.abs(y - ref)
+    assert (d > 1e-2).mean() < 1e-3, (d > 1e-2).mean()
+    assert d.max() < 0.1
+
+
+def test_denoising_reduces_error():
+    x = _noisy((1, 256, 384), 4)
+    H, W = x.shape[-2:]
+    yy, xx = np.mgrid[0:H, 0:W]
+    clean = (0.5 + 0.4 * np.sin(xx / 17.0) * np.cos(yy / 23.0)).astype(np.float32)
+    y = _gpu(x, threshold=0.15)
+    assert np.sqrt(((y[0] - clean) ** 2).mean()) < 0.5 * np.sqrt(((x[0] - clean) ** 2).mean())
