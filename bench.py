@@ -46,6 +46,9 @@ CONFIGS = {
     "c3-15": (4320, 7680, 4320, 7680, "gauss", 15, "c3: 8K RGB bf16 separable Gaussian, 15 taps"),
     "c3-21": (4320, 7680, 4320, 7680, "gauss", 21, "c3: 8K RGB bf16 separable Gaussian, 21 taps"),
     "c3-31": (4320, 7680, 4320, 7680, "gauss", 31, "c3: 8K RGB bf16 separable Gaussian, 31 taps"),
+    "c4": (2160, 3840, 2160, 3840, "dct16", 0,
+           "c4: 4K RGB bf16 DCT-16 transform-domain denoise (16x16 tiles, stride 8, hard coring "
+           "threshold 0.15, windowed overlap-add), one fused kernel, bf16 out"),
     "c5": (2160, 3840, 1080, 1920, "lanczos+gauss", 9,
            "c5: batch of 512 4K RGB bf16 frames -> 1080p Lanczos-3 2x then 9-tap Gaussian "
            "(composed into one fused pass), frame-sharded across GPUs"),
@@ -140,6 +143,8 @@ def make_op(cfg):
         return lambda x: pipelines.resample(x, oh, ow)
     if op == "lanczos+gauss":
         return lambda x: pipelines.resample_filter(x, oh, ow, taps)
+    if op == "dct16":
+        return lambda x: pipelines.denoise_dct16(x, 0.15, "hard")
     return lambda x: pipelines.gaussian_blur(x, taps)
 
 
@@ -293,7 +298,8 @@ def run_b200(args):
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes,
-                         "kernel": "tsb::separable_kernel (fused V+H tcgen05 pass)",
+                         "kernel": ("tsb::dct::dct16_kernel (fused DCT-16 denoise)" if op == "dct16"
+                                    else "tsb::separable_kernel (fused V+H tcgen05 pass)"),
                          "avg_launch_ms": round(launch_ms, 5)},
             "cpu_baseline": cpu,
             "clocks": clk,
@@ -315,6 +321,8 @@ def cpu_baseline(cfg):
         pipelines_ref.resample(img, oh, ow)
     elif op == "lanczos+gauss":
         pipelines_ref.gaussian_blur(pipelines_ref.resample(img, oh, ow), taps)
+    elif op == "dct16":
+        pipelines_ref.dct_denoise(img, 0.15, "hard")
     else:
         pipelines_ref.gaussian_blur(img, taps)
     dt = time.perf_counter() - t

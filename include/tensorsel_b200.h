@@ -137,6 +137,11 @@ TS_API ts_status ts_denoise_dct16(const void* in, int64_t in_row_stride, int64_t
                                   int64_t out_plane_stride, int out_dtype, int planes, int height,
                                   int width, float threshold, int soft, void* stream);
 
+/* Diagnostics: subsequent ts_denoise_dct16 launches copy the TMEM
+ * accumulators of CTA 0's first band (D1, D2, D3 per phase; D4) into
+ * device_buffer (f32[4][2][128][256]); NULL turns it off. */
+TS_API ts_status ts_debug_dct16(float* device_buffer);
+
 /* Elementwise f32 -> bf16 (round to nearest even), n elements. */
 TS_API ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream);
 

@@ -53,6 +53,7 @@ _SIGNATURES = {
     "ts_separable_run": (_I, [_P, _P, _I, _P, _I64, _I64, _I, _P, _I64, _I64, _I, _P]),
     "ts_separable_plan": (_I, [_P, _P, _I, _I, ctypes.POINTER(ctypes.c_int)]),
     "ts_cast_f32_bf16": (_I, [_P, _P, _I64, _P]),
+    "ts_debug_dct16": (_I, [_P]),
     "ts_denoise_dct16": (_I, [_P, _I64, _I64, _I, _P, _I64, _I64, _I, _I, _I, _I,
                               ctypes.c_float, _I, _P]),
     "ts_matrix_for": (_I, [_I, _I, _I, _I, _P, _P, _P]),

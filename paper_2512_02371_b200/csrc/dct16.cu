@@ -12,12 +12,15 @@
 // steps (M=128, N=16), choosing operand majors so no explicit transposes are
 // needed:
 //   S1 (SS, bf16)  D1[c][16i+k]   = Σ_r X[16i+8p+r][c] Dw[k][r]    A = band, MN-major
-//   E1             D1 -> S_Y (f32, MN-major: M = freq-row m, K = col)
-//   S3 (SS, tf32)  D2[m][16(8q+j)+l] = Σ_c Y[m][16j+8q+c] Dw[l][c]
+//   E1             D1 -> S_Y (bf16 hi + lo pair, MN-major: M = freq-row m, K = col)
+//   S3 (SS, bf16)  D2[m][16(8q+j)+l] = Σ_c (Y_hi + Y_lo)[m][16j+8q+c] Dw[l][c]
 //   E2             coring of D2 in TMEM (in place)
 //   S5 (TS, tf32)  D3[m][16j+8q+c] += Σ_l C'[m][..+l] Dw[l][c]     A = D2 from TMEM
-//   E3             D3 -> S_R (f32, MN-major: M = col, K = freq-row)
-//   S7 (SS, tf32)  D4[c][16i+8p+r] += Σ_k R[16i+k][c] Dw[k][r]     (both p accumulate)
+//   E3             D3 -> S_R (bf16 hi + lo, MN-major: M = col, K = freq-row)
+//   S7 (SS, bf16)  D4[c][16i+8p+r] += Σ_k (R_hi + R_lo)[16i+k][c] Dw[k][r]  (both p accumulate)
+// (kind::tf32 does not accept an MN-major A from shared memory on sm_100a —
+// it silently yields zeros, see ts_probe_mma amode 3 — so f32 intermediates
+// travel as bf16 hi/lo pairs, two MMAs per K step, ~16 mantissa bits.)
 // and finally E4: D4 (lane = column, columns = band rows) -> bf16/f32 -> TMA
 // store of the 112x112 block.  Steps run in sequence within a CTA (MMA warp
 // and epilogue warpgroup hand off through mbarriers); the next band's TMA
@@ -45,7 +48,8 @@ constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
 constexpr int kBand = 128;
 constexpr int kOut = 112;
 constexpr uint32_t kBandBytes = kBand * kBand * 2;  // bf16 band, two 64-col SW128 halves
-constexpr uint32_t kOpBytes = 128 * 128 * 4;        // f32 operand (S_Y / S_R alias)
+constexpr uint32_t kOpBytes = 128 * 128 * 4;        // bf16 hi + lo operand (S_Y / S_R alias)
+constexpr uint32_t kOpLo = 128 * 128 * 2;           // offset of the lo half
 
 // smem layout (bytes from the 1024-aligned base)
 constexpr uint32_t kOffX = 0;                           // 2 band buffers
@@ -53,17 +57,37 @@ constexpr uint32_t kOffOp = kOffX + 2 * kBandBytes;     // S_Y / S_R
 constexpr uint32_t kOffOut = kOffOp + kOpBytes;         // 112 x 112 staging (f32 worst case)
 constexpr uint32_t kOutBytes = kOut * kOut * 4;
 constexpr uint32_t kOffB = kOffOut + ((kOutBytes + 1023) / 1024) * 1024;
-// constant B tiles: [0] bf16 Dwᵀ (512 B), [1] f32 Dwᵀ (1 KB), [2] f32 Dw (1 KB)
-constexpr uint32_t kOffB1 = kOffB, kOffB3 = kOffB + 512, kOffB5 = kOffB + 1536;
-constexpr uint32_t kOffBar = kOffB + 2560;
+// constant B tiles: bf16 Dwᵀ hi + lo (S1, S3: the steps whose rounding decides
+// which coefficients are cored) in three edge variants each — 0 interior,
+// 1 "low cut" (samples 0..7 lie outside the image: their weight is folded
+// onto sample 8, clamp-to-edge), 2 "high cut" (8..15 outside, folded onto
+// 7); TMA zero-fills the outside samples — then f32 Dw (S5), bf16 Dw (S7)
+constexpr uint32_t kOffB1 = kOffB, kOffB1L = kOffB + 1536, kOffB5 = kOffB + 3072,
+                   kOffB7 = kOffB + 4096;
+constexpr uint32_t kConstBytes = 4608;
+constexpr uint32_t kOffBar = kOffB + kConstBytes;
 constexpr uint32_t kSmem = kOffBar + 256 + 1024;
 
 struct Params {
   int planes, H, W, nry, nrx, nregions;
   float threshold;
   int soft;                 // 0 hard, 1 soft coring
-  const uint8_t* consts;    // 2560 bytes: the three B tiles in smem layout
+  const uint8_t* consts;    // kConstBytes: the three B tiles in smem layout
+  float* dbg;               // diagnostics: [4 stages][2 phases][128 lanes][256] for CTA 0, band 0
 };
+
+// Diagnostics: copy `ncols` TMEM columns of this thread's lane to dbg.
+__device__ __forceinline__ void dbg_dump(const Params& P, int it, int stage, int p, uint32_t taddr,
+                                         int row, int ncols) {
+  if (P.dbg == nullptr || blockIdx.x != 0 || it != 0) return;
+  float* dst = P.dbg + ((static_cast<size_t>(stage) * 2 + p) * 128 + row) * 256;
+  for (int c0 = 0; c0 < ncols; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(taddr + c0, r);
+    tmem_wait_ld();
+    for (int i = 0; i < 16; ++i) dst[c0 + i] = __uint_as_float(r[i]);
+  }
+}
 
 __device__ __forceinline__ void mma_tf32_ss_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                                   uint32_t acc) {
@@ -93,12 +117,39 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
-// f32 MN-major 128B-swizzled operand: M = 128 (4 atoms of 32), K = 128 (16
-// groups of 8 at 1 KB); element (m, k)
-__device__ __forceinline__ uint32_t opf32_chunk(uint32_t base, int m4, int k) {
-  // address of the 16-byte chunk holding m = 4*m4 .. 4*m4+3 at row k
-  return base + (m4 / 8) * 16384u + (k / 8) * 1024u + (k % 8) * 128u +
-         ((((m4 % 8) ^ (k % 8))) * 16u);
+// bf16 MN-major 128B-swizzled operand: M = 128 (2 atoms of 64 at 16 KB),
+// K = 128 (16 groups of 8 rows at 1 KB).  Address of the 16-byte chunk
+// holding m = 8*m8 .. 8*m8+7 at K row k.
+__device__ __forceinline__ uint32_t opbf_chunk(uint32_t base, int m8, int k) {
+  return base + (m8 / 8) * 16384u + (k / 8) * 1024u + (k % 8) * 128u +
+         ((((m8 % 8) ^ (k % 8))) * 16u);
+}
+
+// Write 16 consecutive-M f32 values of K row k as bf16 hi/lo pairs.
+__device__ __forceinline__ void put_hilo16(uint32_t op_s, int m8_first, int k,
+                                           const uint32_t (&r)[16]) {
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float a = __uint_as_float(r[8 * g + 2 * e]), b = __uint_as_float(r[8 * g + 2 * e + 1]);
+      const __nv_bfloat16 ah = __float2bfloat16_rn(a), bh = __float2bfloat16_rn(b);
+      hi[e] = pack_bf16x2(a, b);
+      lo[e] = pack_bf16x2(a - __bfloat162float(ah), b - __bfloat162float(bh));
+    }
+    const uint32_t addr = opbf_chunk(op_s, m8_first + g, k);
+    st_shared_v4(addr, hi[0], hi[1], hi[2], hi[3]);
+    st_shared_v4(addr + kOpLo, lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// Edge variant of a 16-sample tile starting at image coordinate x0 (multiple
+// of 8) on an axis of length n (multiple of 8).
+__device__ __forceinline__ uint32_t edge_variant(int x0, int n) {
+  if (x0 < 0 && x0 + 16 > 0) return 1u;
+  if (x0 < n && x0 + 16 > n) return 2u;
+  return 0u;
 }
 
 struct Region {
@@ -112,36 +163,6 @@ __device__ __forceinline__ Region region_of(const Params& P, int t) {
   r.ry = rest % P.nry;
   r.p = rest / P.nry;
   return r;
-}
-
-// Replicate the image edge into the out-of-image rows/cols of a band
-// (TMA zero-filled them).  band row b <-> image row Y-8+b, col c <-> X-8+c.
-__device__ void fixup_band(uint8_t* band, int Y, int X, int H, int W, int lane) {
-  auto at = [&](int r, int c) -> __nv_bfloat16* {
-    const int half = c / 64, cc = c % 64;
-    const uint32_t off = half * (kBand * 128u) + r * 128u + ((((cc / 8) ^ (r % 8))) * 16u) +
-                         (cc % 8) * 2u;
-    return reinterpret_cast<__nv_bfloat16*>(band + off);
-  };
-  const int r_lo = max(0, 8 - Y);                        // first band row inside the image
-  const int r_hi = min(kBand, H - (Y - 8));              // one past the last
-  const int c_lo = max(0, 8 - X);
-  const int c_hi = min(kBand, W - (X - 8));
-  if (r_lo == 0 && r_hi == kBand && c_lo == 0 && c_hi == kBand) return;
-  // columns first (rows inside the image), then full rows from the nearest valid row
-  for (int e = lane; e < kBand * kBand; e += 32) {
-    const int r = e / kBand, c = e % kBand;
-    if (r < r_lo || r >= r_hi) continue;
-    if (c < c_lo) *at(r, c) = *at(r, c_lo);
-    else if (c >= c_hi) *at(r, c) = *at(r, c_hi - 1);
-  }
-  __syncwarp();
-  for (int e = lane; e < kBand * kBand; e += 32) {
-    const int r = e / kBand, c = e % kBand;
-    if (r < r_lo) *at(r, c) = *at(r_lo, c);
-    else if (r >= r_hi) *at(r, c) = *at(r_hi - 1, c);
-  }
-  __syncwarp();
 }
 
 template <typename OutT>
@@ -196,8 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_arrive_expect_tx(cbar, 2560);
-      bulk_g2s(base + kOffB, P.consts, 2560, cbar);
+      mbar_arrive_expect_tx(cbar, kConstBytes);
+      bulk_g2s(base + kOffB, P.consts, kConstBytes, cbar);
       int it = 0;
       for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
         const int s = it & 1;
@@ -213,13 +234,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t id_bf = make_idesc(kFmtBF16, 128, 16, /*A MN*/ 1, 0);
-    const uint32_t id_tf_mn = make_idesc(kFmtTF32, 128, 16, 1, 0);
     const uint32_t id_tf_k = make_idesc(kFmtTF32, 128, 16, 0, 0);
     // B descriptors (K-major, no swizzle): bf16 16x16 (LBO 128, SBO 256);
     // f32 16x16 (core matrices 8 n x 4 k: LBO 128, SBO 512)
     const uint64_t bd1 = make_sdesc(base_s + kOffB1, 128u, 256u, kSwizzleNone);
-    const uint64_t bd3 = make_sdesc(base_s + kOffB3, 128u, 512u, kSwizzleNone);
+    const uint64_t bd1l = make_sdesc(base_s + kOffB1L, 128u, 256u, kSwizzleNone);
     const uint64_t bd5 = make_sdesc(base_s + kOffB5, 128u, 512u, kSwizzleNone);
+    const uint64_t bd7 = make_sdesc(base_s + kOffB7, 128u, 256u, kSwizzleNone);
     const uint32_t op_s = base_s + kOffOp;
     mbar_wait(cbar, 0);
     int it = 0;
@@ -229,10 +250,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Region R = region_of(P, t);
       const int Y = R.ry * kOut, X = R.rx * kOut;
       mbar_wait(&xfull[s], (it >> 1) & 1);
-      uint8_t* band = base + kOffX + s * kBandBytes;
-      fixup_band(band, Y, X, P.H, P.W, lane);
-      fence_proxy_async_smem();
-      __syncwarp();
       const uint32_t band_s = base_s + kOffX + s * kBandBytes;
       for (int p = 0; p < 2; ++p) {
         const int ni = p == 0 ? 8 : 7;
@@ -242,23 +259,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < ni; ++i) {
           const uint64_t ad =
               make_sdesc(band_s + (16u * i + 8u * p) * 128u, kBand * 128u, 1024u, kSwizzle128B);
-          mma_f16_ss_elect(tD1 + 16u * i, ad, bd1, id_bf, 0u);
+          const uint32_t v = edge_variant(Y - 8 + 16 * i + 8 * p, P.H);
+          mma_f16_ss_elect(tD1 + 16u * i, ad, bd1 + 32u * v, id_bf, 0u);
+          mma_f16_ss_elect(tD1 + 16u * i, ad, bd1l + 32u * v, id_bf, 1u);
         }
         mma_commit_elect(b_s1);
         if (p == 1) mma_commit_elect(&xempty[s]);
-        // ---- S3: row forward (A = S_Y f32 MN-major: M = freq-row, K = col)
+        // ---- S3: row forward (A = S_Y hi/lo MN-major: M = freq-row, K = col)
         mbar_wait(e1, ph_e);
         tc_fence_after();
         for (int q = 0; q < 2; ++q) {
           const int nj = q == 0 ? 8 : 7;
           for (int j = 0; j < nj; ++j) {
             const uint32_t kc = 16u * j + 8u * q;  // first column of the tile
-            for (int h = 0; h < 2; ++h) {
-              const uint64_t ad =
-                  make_sdesc(op_s + ((kc / 8u) + h) * 1024u, 16384u, 1024u, kSwizzle128B);
-              mma_tf32_ss_elect(tD2 + 16u * (8 * q + j), ad, bd3 + 16u * h, id_tf_mn,
-                                h ? 1u : 0u);
-            }
+            const uint64_t ad = make_sdesc(op_s + (kc / 8u) * 1024u, 16384u, 1024u, kSwizzle128B);
+            const uint64_t adl =
+                make_sdesc(op_s + kOpLo + (kc / 8u) * 1024u, 16384u, 1024u, kSwizzle128B);
+            const uint32_t v = edge_variant(X - 8 + static_cast<int>(kc), P.W);
+            mma_f16_ss_elect(tD2 + 16u * (8 * q + j), ad, bd1 + 32u * v, id_bf, 0u);
+            mma_f16_ss_elect(tD2 + 16u * (8 * q + j), adl, bd1 + 32u * v, id_bf, 1u);
+            mma_f16_ss_elect(tD2 + 16u * (8 * q + j), ad, bd1l + 32u * v, id_bf, 1u);
           }
         }
         mma_commit_elect(b_s3);
@@ -275,17 +295,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         mma_commit_elect(b_s5);
-        // ---- S7: column inverse (A = S_R f32 MN-major: M = col, K = freq-row)
+        // ---- S7: column inverse (A = S_R hi/lo MN-major: M = col, K = freq-row)
         mbar_wait(e3, ph_e);
         if (p == 0 && it > 0) mbar_wait(e4, (it - 1) & 1);  // previous E4 read D4
         tc_fence_after();
         for (int i = 0; i < ni; ++i) {
-          for (int h = 0; h < 2; ++h) {
-            const uint64_t ad =
-                make_sdesc(op_s + (2u * i + h) * 1024u, 16384u, 1024u, kSwizzle128B);
-            mma_tf32_ss_elect(tD4 + 16u * i + 8u * p, ad, bd5 + 16u * h, id_tf_mn,
-                              (p > 0 || h > 0) ? 1u : 0u);
-          }
+          const uint64_t ad = make_sdesc(op_s + (2u * i) * 1024u, 16384u, 1024u, kSwizzle128B);
+          const uint64_t adl =
+              make_sdesc(op_s + kOpLo + (2u * i) * 1024u, 16384u, 1024u, kSwizzle128B);
+          mma_f16_ss_elect(tD4 + 16u * i + 8u * p, ad, bd7, id_bf, p > 0 ? 1u : 0u);
+          mma_f16_ss_elect(tD4 + 16u * i + 8u * p, adl, bd7, id_bf, 1u);
         }
         mma_commit_elect(b_s7);
         ph_e ^= 1;
@@ -307,14 +326,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- E1: D1 (lane = col c) -> S_Y[m][c] f32 MN-major (M = m, K = c)
         mbar_wait(b_s1, ph);
         tc_fence_after();
+        dbg_dump(P, it, 0, p, tD1 + lane_off, row, 128);
         for (int ch = 0; ch < 8; ++ch) {
           uint32_t r[16];
           tmem_ld16(tD1 + lane_off + 16u * ch, r);
           tmem_wait_ld();
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            st_shared_v4(opf32_chunk(op_s, ch * 4 + g, row), r[4 * g], r[4 * g + 1], r[4 * g + 2],
-                         r[4 * g + 3]);
+          put_hilo16(op_s, 2 * ch, row, r);  // M = freq-row 16ch.., K = this column
         }
         tc_fence_before();
         fence_proxy_async_smem();
@@ -322,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- E2: coring of D2 (lane = freq-row m, cols = 16*(8q+j) + l) in place
         mbar_wait(b_s3, ph);
         tc_fence_after();
+        dbg_dump(P, it, 1, p, tD2 + lane_off, row, 240);
         for (int ch = 0; ch < 15; ++ch) {
           uint32_t r[16];
           tmem_ld16(tD2 + lane_off + 16u * ch, r);
@@ -346,14 +364,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- E3: D3 (lane = m, cols = band col c) -> S_R[c][m] f32 MN-major (M = c, K = m)
         mbar_wait(b_s5, ph);
         tc_fence_after();
+        dbg_dump(P, it, 2, p, tD3 + lane_off, row, 128);
         for (int ch = 0; ch < 8; ++ch) {
           uint32_t r[16];
           tmem_ld16(tD3 + lane_off + 16u * ch, r);
           tmem_wait_ld();
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            st_shared_v4(opf32_chunk(op_s, ch * 4 + g, row), r[4 * g], r[4 * g + 1], r[4 * g + 2],
-                         r[4 * g + 3]);
+          put_hilo16(op_s, 2 * ch, row, r);  // M = band col 16ch.., K = this freq-row
         }
         tc_fence_before();
         fence_proxy_async_smem();
@@ -364,6 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // ---- E4: D4 (lane = band col c, cols = band row) -> output block
       tc_fence_after();
+      dbg_dump(P, it, 3, 0, tD4 + lane_off, row, 128);
       if (et == 0) bulk_wait_read0();
       named_bar_sync(1, 128);
       OutT* stg = reinterpret_cast<OutT*>(base + kOffOut);
@@ -406,6 +423,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace dct
 
+static float* g_dct_dbg = nullptr;
+void dct_set_debug(float* p) { g_dct_dbg = p; }
+
 // Host: the constant B tiles in their smem byte layout.
 static void build_consts(uint8_t* out) {
   double D[16][16], w[16];
@@ -414,25 +434,51 @@ static void build_consts(uint8_t* out) {
     for (int m = 0; m < 16; ++m)
       D[k][m] = std::cos(3.14159265358979323846 * (2 * m + 1) * k / 32.0) *
                 std::sqrt((k == 0 ? 1.0 : 2.0) / 16.0) * w[m];
-  // [0,512): bf16 B1[K=r][N=k] = Dw[k][r], K-major core matrices (8 n x 8 k)
-  for (int kk = 0; kk < 16; ++kk)
-    for (int n = 0; n < 16; ++n) {
-      const float v = static_cast<float>(D[n][kk]);
-      uint32_t b;
-      std::memcpy(&b, &v, 4);
-      const uint16_t h = static_cast<uint16_t>((static_cast<uint64_t>(b) + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
-      const int off = (n / 8) * 256 + (kk / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2;
-      std::memcpy(out + off, &h, 2);
-    }
+  auto bf16_bits = [](double v) {
+    const float f = static_cast<float>(v);
+    uint32_t b;
+    std::memcpy(&b, &f, 4);
+    return static_cast<uint16_t>((static_cast<uint64_t>(b) + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+  };
+  auto bf16_val = [](uint16_t h) {
+    const uint32_t b = static_cast<uint32_t>(h) << 16;
+    float f;
+    std::memcpy(&f, &b, 4);
+    return static_cast<double>(f);
+  };
+  // lo = 0: bf16(v); lo = 1: bf16(v - bf16(v))
+  auto put16 = [&](uint8_t* dst, int kk, int n, double v, int lo) {
+    uint16_t h = bf16_bits(v);
+    if (lo) h = bf16_bits(v - bf16_val(h));
+    std::memcpy(dst + (n / 8) * 256 + (kk / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2, &h, 2);
+  };
   // f32 K-major core matrices (8 n x 4 k): (n/8)*512 + (k/4)*128 + (n%8)*16 + (k%4)*4
   auto put32 = [&](uint8_t* dst, int kk, int n, double v) {
     const float f = static_cast<float>(v);
     std::memcpy(dst + (n / 8) * 512 + (kk / 4) * 128 + (n % 8) * 16 + (kk % 4) * 4, &f, 4);
   };
+  for (int v = 0; v < 3; ++v) {
+    // B1[K = sample][N = freq] = Dw[freq][sample], edge-folded (variant v)
+    double F[16][16];
+    for (int n = 0; n < 16; ++n)
+      for (int kk = 0; kk < 16; ++kk) F[n][kk] = D[n][kk];
+    for (int n = 0; n < 16; ++n) {
+      if (v == 1) {
+        for (int kk = 0; kk < 8; ++kk) { F[n][8] += F[n][kk]; F[n][kk] = 0; }
+      } else if (v == 2) {
+        for (int kk = 8; kk < 16; ++kk) { F[n][7] += F[n][kk]; F[n][kk] = 0; }
+      }
+    }
+    for (int kk = 0; kk < 16; ++kk)
+      for (int n = 0; n < 16; ++n) {
+        put16(out + 512 * v, kk, n, F[n][kk], 0);         // hi
+        put16(out + 1536 + 512 * v, kk, n, F[n][kk], 1);  // lo
+      }
+  }
   for (int kk = 0; kk < 16; ++kk)
     for (int n = 0; n < 16; ++n) {
-      put32(out + 512, kk, n, D[n][kk]);   // B3[K=c][N=l] = Dw[l][c]
-      put32(out + 1536, kk, n, D[kk][n]);  // B5[K=l][N=c] = Dw[l][c]
+      put32(out + 3072, kk, n, D[kk][n]);    // B5[K=l][N=c] = Dw[l][c] (S5, f32)
+      put16(out + 4096, kk, n, D[kk][n], 0); // B7[K=k][N=r] = Dw[k][r] (S7)
     }
 }
 
@@ -454,11 +500,11 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return set_error(TS_ERR_INVALID, "dct16: device index");
   if (!d_consts[dev]) {
-    uint8_t h[2560] = {0};
+    uint8_t h[dct::kConstBytes] = {0};
     build_consts(h);
-    cudaError_t e = cudaMalloc(&d_consts[dev], 2560);
+    cudaError_t e = cudaMalloc(&d_consts[dev], dct::kConstBytes);
     if (e != cudaSuccess) return cuda_error(e, "dct16 consts");
-    e = cudaMemcpy(d_consts[dev], h, 2560, cudaMemcpyHostToDevice);
+    e = cudaMemcpy(d_consts[dev], h, dct::kConstBytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_error(e, "dct16 consts copy");
   }
   dct::Params P;
@@ -471,6 +517,7 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
   P.threshold = threshold;
   P.soft = soft;
   P.consts = d_consts[dev];
+  P.dbg = g_dct_dbg;
   CUtensorMap tin, tout;
   ts_status st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs,
                                 in_ps, 64, dct::kBand, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -500,6 +547,11 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
 }
 
 }  // namespace tsb
+
+extern "C" ts_status ts_debug_dct16(float* device_buffer) {
+  tsb::dct_set_debug(device_buffer);
+  return TS_OK;
+}
 
 extern "C" ts_status ts_denoise_dct16(const void* in, int64_t in_row_stride, int64_t in_plane_stride,
                                       int in_dtype, void* out, int64_t out_row_stride,

@@ -44,9 +44,10 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t raw_s = smem_u32(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_s - raw_s);
-  const bool tf32 = amode == 2;
+  const bool tf32 = amode >= 2;
+  const bool a_tmem = amode == 2;
   const int es = tf32 ? 4 : 2;
-  const uint32_t a_bytes = tf32 ? 0u : 128u * k * 2u;
+  const uint32_t a_bytes = a_tmem ? 0u : 128u * k * (tf32 ? 4u : 2u);
   const uint32_t b_bytes = static_cast<uint32_t>(k) * n * es;
   uint8_t* sa = base;
   uint8_t* sb = base + a_bytes;
@@ -57,6 +58,19 @@ __global__ void __launch_bounds__(128, 1)
   // ---- stage A
   const uint32_t lbo_a_mn = static_cast<uint32_t>(k / 8) * 1024u;  // m-atom stride (amode 0)
   const uint32_t sbo_a_k = static_cast<uint32_t>(k / 8) * 128u;    // 8-row group stride (amode 1)
+  if (amode == 3 || amode == 4) {
+    for (int e = threadIdx.x; e < 128 * k; e += blockDim.x) {
+      const int m = e / k, kk = e % k;
+      uint32_t off;
+      if (amode == 3)  // MN-major SW128: 32 f32 per atom row, k rows at 128 B
+        off = (m / 32) * (static_cast<uint32_t>(k / 8) * 1024u) + (kk / 8) * 1024u +
+              (kk % 8) * 128u + ((((m % 32) / 4) ^ (kk % 8)) * 16u) + (m % 4) * 4u;
+      else  // K-major no swizzle: core matrices 8 m x 4 k
+        off = (m / 8) * (static_cast<uint32_t>(k / 4) * 128u) + (kk / 4) * 128u + (m % 8) * 16u +
+              (kk % 4) * 4u;
+      *reinterpret_cast<float*>(sa + off) = a[e];
+    }
+  }
   if (!tf32) {
     for (int e = threadIdx.x; e < 128 * k; e += blockDim.x) {
       const int m = e / k, kk = e % k;
@@ -99,7 +113,7 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tmem = *slot;
   const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
 
-  if (tf32) {
+  if (a_tmem) {
     // A row m = this thread's TMEM lane, columns [256, 256 + k)
     const int m = warp * 32 + lane;
     for (int c0 = 0; c0 < k; c0 += 16) {
@@ -116,7 +130,8 @@ __global__ void __launch_bounds__(128, 1)
   long long t0 = 0, t1 = 0;
   if (threadIdx.x == 0) {
     const uint32_t idesc =
-        make_idesc(tf32 ? kFmtTF32 : kFmtBF16, 128, n, amode == 0 ? 1u : 0u, bmode == 1 ? 1u : 0u);
+        make_idesc(tf32 ? kFmtTF32 : kFmtBF16, 128, n, (amode == 0 || amode == 3) ? 1u : 0u,
+                   bmode == 1 ? 1u : 0u);
     const int kstep = tf32 ? 8 : 16;
     t0 = clock64();
     for (int r = 0; r < reps; ++r) {
@@ -128,7 +143,17 @@ __global__ void __launch_bounds__(128, 1)
         if (tf32) {
           const uint64_t bd = make_sdesc(base_s + a_bytes + q * 256u, 128u,
                                          static_cast<uint32_t>(k / 4) * 128u, kSwizzleNone);
-          mma_tf32_ts(tmem + dcol, tmem + 256u + q * 8u, bd, idesc, acc);
+          if (amode == 2) {
+            mma_tf32_ts(tmem + dcol, tmem + 256u + q * 8u, bd, idesc, acc);
+          } else {
+            const uint64_t ad =
+                amode == 3
+                    ? make_sdesc(base_s + q * 1024u, static_cast<uint32_t>(k / 8) * 1024u, 1024u,
+                                 kSwizzle128B)
+                    : make_sdesc(base_s + q * 256u, 128u, static_cast<uint32_t>(k / 4) * 128u,
+                                 kSwizzleNone);
+            mma_tf32_ss(tmem + dcol, ad, bd, idesc, acc);
+          }
         } else {
           const uint64_t ad =
               amode == 0 ? make_sdesc(base_s + q * 2048u, lbo_a_mn, 1024u, kSwizzle128B)
@@ -171,13 +196,13 @@ using namespace tsb;
 extern "C" ts_status ts_probe_mma(int amode, int bmode, const float* a, const float* b, float* d,
                                   int k, int n, int reps, long long* cycles, int nacc,
                                   void* stream) {
-  const int kstep = amode == 2 ? 8 : 16;
-  if (amode < 0 || amode > 2 || bmode < 0 || bmode > 1 || (amode == 2 && bmode != 0) || !a ||
+  const int kstep = amode >= 2 ? 8 : 16;
+  if (amode < 0 || amode > 4 || bmode < 0 || bmode > 1 || (amode >= 2 && bmode != 0) || !a ||
       !b || !d || k < kstep || k > 256 || k % 16 || n < 16 || n > 256 || n % 16 || reps < 1 ||
-      nacc < 1 || nacc * n > (amode == 2 ? 256 : 512))
+      nacc < 1 || nacc * n > (amode == 2 ? 256 : 512) || (amode >= 3 && k > 128))
     return set_error(TS_ERR_INVALID, "probe_mma: bad arguments");
-  const int es = amode == 2 ? 4 : 2;
-  const uint32_t a_bytes = amode == 2 ? 0u : 128u * k * 2u;
+  const int es = amode >= 2 ? 4 : 2;
+  const uint32_t a_bytes = amode == 2 ? 0u : 128u * k * (amode >= 3 ? 4u : 2u);
   const uint32_t b_bytes = static_cast<uint32_t>(k) * n * es;
   const uint32_t smem = 1024 + a_bytes + ((b_bytes + 1023u) & ~1023u) + 64;
   cudaError_t e =

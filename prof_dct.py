@@ -1,0 +1,5 @@
+import torch
+from paper_2512_02371_b200 import pipelines
+x = torch.rand((3, 2160, 3840), device="cuda").bfloat16()
+for _ in range(3): y = pipelines.denoise_dct16(x, 0.15)
+torch.cuda.synchronize(); print("ok")
