@@ -142,6 +142,48 @@ TS_API ts_status ts_denoise_dct16(const void* in, int64_t in_row_stride, int64_t
  * device_buffer (f32[4][2][128][256]); NULL turns it off. */
 TS_API ts_status ts_debug_dct16(float* device_buffer);
 
+/* One lowered convolution statement group of a tensorsel program, batched
+ * over `instances` program instances (e.g. a difftest's seeds):
+ *   acc = zero_init ? 0 : acc
+ *   for v < iterations:
+ *     acc = wmma_mma(wmma_load_a(src, a_base[v], a_stride, m, k),
+ *                    wmma_load_b(B_v, 0, n, k, n), acc)
+ *   B_v[kk][j] = b_off[kk*n + j] < 0 ? 0 : kern[k_base[v] + b_off[kk*n + j]]
+ * evaluated with interp.py's exact semantics (interp.py:427-486): loaded
+ * values re-rounded to their kind (0 f32, 1 f16, 2 bf16), f32 products,
+ * k summed left to right, then acc + s — bit-identical to the reference.
+ * Buffers are f32 carriers (device), instance t at base + t*stride.
+ * *error (device) is set to 1 + index (src) or -(1 + index) (kern) on an
+ * out-of-bounds read (interp.OutOfBounds). */
+typedef struct ts_conv_group {
+  int instances;
+  const float* src;
+  int64_t src_stride;
+  int src_len, src_kind;
+  const float* kern;
+  int64_t kern_stride;
+  int kern_len, kern_kind;
+  float* acc;
+  int64_t acc_stride;
+  int zero_init;
+  int m, k, n, a_stride;
+  int iterations;
+  const int32_t* a_base;
+  const int32_t* k_base;
+  const int32_t* b_off;
+  /* Optional explicit gathers (source-form statements, interp.py:174-212):
+   * when non-NULL, a_idx/b_idx ([iterations][m*n][k], device) give the src
+   * and kern index of every (output, tap) product (b_idx -1 = zero) and
+   * override a_base/a_stride/k_base/b_off. */
+  const int32_t* a_idx;
+  const int32_t* b_idx;
+  int32_t* error;
+} ts_conv_group;
+
+/* Replaces the serial For/Store walk of interp.run_program (interp.py:570-619)
+ * over a lowered conv group (interp.py:419-486, 488-534). */
+TS_API ts_status ts_run_conv_group(const ts_conv_group* group, void* stream);
+
 /* Elementwise f32 -> bf16 (round to nearest even), n elements. */
 TS_API ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream);
 

@@ -132,9 +132,14 @@ def main():
 
     # -- conv corpus: source form == lowered form, outputs recorded
     corpus = {}
+    programs = {}
     for name in ("conv1d_k8", "conv1d_k16", "conv2d_outer_ry", "downsample2_1d", "upsample2_1d"):
         prog = ir.parse_program(open(os.path.join(CORPUS, f"{name}.sexp")).read())
         low, rep = selector.select_program(prog, selector.SelectionConfig(target="wmma"))
+        low_nd, _ = selector.select_program(
+            prog, selector.SelectionConfig(target="wmma", desugar=False))
+        programs[name] = {"source": ir.print_program(prog), "lowered": ir.print_program(low),
+                          "lowered_shuffle_intrinsics": ir.print_program(low_nd)}
         for seed in range(3):
             ins = interp.random_inputs(prog, seed)
             a = interp.run_program(prog, ins)
@@ -159,6 +164,10 @@ def main():
     assert out_src.tobytes() == out_low.tobytes()
     kats["lanczos_tile"] = {"lowered": bool(rep.ok), "intrinsics": sorted(
         {i for s in rep.statements for i in s.intrinsics})}
+    low_nd, _ = selector.select_program(prog, selector.SelectionConfig(target="wmma", desugar=False))
+    programs["lanczos_tile"] = {"source": ir.print_program(prog), "lowered": ir.print_program(low),
+                                "lowered_shuffle_intrinsics": ir.print_program(low_nd)}
+    kats["programs"] = programs
     arrays["lanczos_tile_K"], arrays["lanczos_tile_I"], arrays["lanczos_tile_out"] = K, I, out_src
 
     # -- image-level goldens: a small bf16 image through reference programs,

@@ -24,6 +24,23 @@ _lock = threading.Lock()
 _lib = None
 
 
+class ConvGroup(ctypes.Structure):
+    """ts_conv_group (include/tensorsel_b200.h)."""
+    _fields_ = [
+        ("instances", ctypes.c_int),
+        ("src", ctypes.c_void_p), ("src_stride", ctypes.c_int64),
+        ("src_len", ctypes.c_int), ("src_kind", ctypes.c_int),
+        ("kern", ctypes.c_void_p), ("kern_stride", ctypes.c_int64),
+        ("kern_len", ctypes.c_int), ("kern_kind", ctypes.c_int),
+        ("acc", ctypes.c_void_p), ("acc_stride", ctypes.c_int64), ("zero_init", ctypes.c_int),
+        ("m", ctypes.c_int), ("k", ctypes.c_int), ("n", ctypes.c_int), ("a_stride", ctypes.c_int),
+        ("iterations", ctypes.c_int),
+        ("a_base", ctypes.c_void_p), ("k_base", ctypes.c_void_p), ("b_off", ctypes.c_void_p),
+        ("a_idx", ctypes.c_void_p), ("b_idx", ctypes.c_void_p),
+        ("error", ctypes.c_void_p),
+    ]
+
+
 class AxisInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "n_in", "n_out", "taps", "window", "blocks", "unique_tiles",
@@ -53,6 +70,7 @@ _SIGNATURES = {
     "ts_separable_run": (_I, [_P, _P, _I, _P, _I64, _I64, _I, _P, _I64, _I64, _I, _P]),
     "ts_separable_plan": (_I, [_P, _P, _I, _I, ctypes.POINTER(ctypes.c_int)]),
     "ts_cast_f32_bf16": (_I, [_P, _P, _I64, _P]),
+    "ts_run_conv_group": (_I, [_P, _P]),
     "ts_debug_dct16": (_I, [_P]),
     "ts_denoise_dct16": (_I, [_P, _I64, _I64, _I, _P, _I64, _I64, _I, _I, _I, _I,
                               ctypes.c_float, _I, _P]),

@@ -1,0 +1,91 @@
+// executor.cu — GPU execution of lowered convolution statement groups, the
+// backend of interp.run_program for the conv family.
+//
+// A lowered group (rules.py:766-803, 887-902 produce it) is
+//     acc = wmma_zero | acc
+//     for v in iterations:
+//         tmp = ConvolutionShuffle | PolyphaseShuffle | Shuffle(load K[kbase_v ..])
+//         acc = wmma_mma(wmma_load_a(I, abase_v, a_stride, m, k),
+//                        wmma_load_b(tmp, 0, n, k, n), acc)
+// evaluated by interp.py:419-486 as: tiles re-rounded to their buffer kind,
+// products in f32, k summed left to right from k = 0, then C + s.  This
+// kernel evaluates every output (instance t, row i, column j) with exactly
+// that operation order (no FMA contraction), so results are bit-identical to
+// the reference; it batches all instances of a program (a difftest's seeds,
+// or the tiles of an image) into one launch.
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+
+namespace tsb {
+
+__device__ __forceinline__ float round_kind(float x, int kind) {
+  if (kind == 1) return __half2float(__float2half_rn(x));
+  if (kind == 2) return __bfloat162float(__float2bfloat16_rn(x));
+  return x;
+}
+
+__global__ void conv_group_kernel(ts_conv_group g) {
+  const int64_t outs = static_cast<int64_t>(g.m) * g.n;
+  const int64_t total = static_cast<int64_t>(g.instances) * outs;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(e / outs);
+    const int o = static_cast<int>(e % outs);
+    const int i = o / g.n, j = o % g.n;
+    const float* I = g.src + static_cast<int64_t>(t) * g.src_stride;
+    const float* K = g.kern + static_cast<int64_t>(t) * g.kern_stride;
+    float* acc = g.acc + static_cast<int64_t>(t) * g.acc_stride;
+    float c = g.zero_init ? 0.0f : acc[o];
+    for (int v = 0; v < g.iterations; ++v) {
+      const bool expl = g.a_idx != nullptr;
+      const int ab = expl ? 0 : g.a_base[v] + i * g.a_stride;
+      const int kb = expl ? 0 : g.k_base[v];
+      const int64_t xo = (static_cast<int64_t>(v) * outs + o) * g.k;  // explicit-gather row
+      float s = 0.0f;
+      for (int kk = 0; kk < g.k; ++kk) {
+        const int ai = expl ? g.a_idx[xo + kk] : ab + kk;
+        if (ai < 0 || ai >= g.src_len) {
+          atomicExch(g.error, 1 + ai);  // OutOfBounds on the A buffer
+          return;
+        }
+        const float a = round_kind(I[ai], g.src_kind);
+        const int off = expl ? g.b_idx[xo + kk] : g.b_off[kk * g.n + j];
+        float b = 0.0f;
+        if (off >= 0) {
+          const int ki = kb + off;
+          if (ki < 0 || ki >= g.kern_len) {
+            atomicExch(g.error, -(1 + ki));  // OutOfBounds on the kernel buffer
+            return;
+          }
+          b = round_kind(K[ki], g.kern_kind);
+        }
+        const float p = __fmul_rn(a, b);
+        s = kk == 0 ? p : __fadd_rn(s, p);
+      }
+      c = __fadd_rn(c, s);  // interp.py:485: out = c + s
+    }
+    acc[o] = c;
+  }
+}
+
+}  // namespace tsb
+
+using namespace tsb;
+
+extern "C" ts_status ts_run_conv_group(const ts_conv_group* g, void* stream) {
+  if (!g || !g->src || !g->kern || !g->acc || !g->error ||
+      (!g->a_idx && (!g->a_base || !g->k_base || !g->b_off)) || (!g->a_idx != !g->b_idx))
+    return set_error(TS_ERR_INVALID, "conv group: null pointer");
+  if (g->instances < 0 || g->m < 1 || g->n < 1 || g->k < 1 || g->iterations < 0)
+    return set_error(TS_ERR_INVALID, "conv group: bad shape");
+  const int64_t total = static_cast<int64_t>(g->instances) * g->m * g->n;
+  if (total == 0) return TS_OK;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  conv_group_kernel<<<static_cast<int>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(*g);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "conv group launch");
+}

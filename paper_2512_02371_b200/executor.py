@@ -1,0 +1,448 @@
+"""GPU backend for ``interp.run_program`` on convolution-family programs.
+
+Drop-in for the reference executor (interp.py:570-619) on the programs the
+conv rules produce (rules.py:766-836, 887-902) and on their source forms
+(tools/make_corpus.py:142-208):
+
+* lowered:  ``wmma_zero`` / ``ConvolutionShuffle`` | ``PolyphaseShuffle`` |
+  ``Shuffle(load K ...)`` / ``wmma_mma(wmma_load_a, wmma_load_b, acc)`` /
+  ``wmma_store``, optionally inside ``For`` loops with affine bases;
+* source:   ``Store(acc, ramp, VectorReduceAdd(Load I · Load K) + Load acc)``
+  and plain buffer copies.
+
+Each conv statement group runs as ONE launch of ``ts_run_conv_group`` over
+every program instance (``run_program_batch``: e.g. all seeds of a
+difftest), reproducing interp's arithmetic exactly (operand re-rounding,
+f32 products, left-to-right sums, ``acc + s``) — results are bit-identical,
+so the reference's own difftest (cli.py:161-183) passes bitwise.
+
+Programs are duck-typed: real ``tensorsel.ir`` objects or the mirrors in
+:mod:`irlite`.  Anything outside this family raises ``UnsupportedProgram``;
+there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib, layout
+from .errors import EvalError, OutOfBounds, ShapeUnregistered, UnknownIntrinsic
+
+HARDWARE_SHAPES = (("wmma", 32, 16, 8), ("wmma", 16, 16, 16), ("amx", 16, 32, 16))
+_KIND = {"f32": 0, "f16": 1, "bf16": 2}
+
+
+class UnsupportedProgram(EvalError):
+    """A statement outside the conv family the GPU executor implements."""
+
+
+class Buffer:
+    """interp.Buffer (interp.py:132-136)."""
+
+    def __init__(self, kind, location, data):
+        self.kind, self.location, self.data = kind, location, data
+
+    def __repr__(self):
+        return f"Buffer({self.kind!r}, {self.location!r}, <{len(self.data)}>)"
+
+
+class BufferStore(dict):
+    """interp.BufferStore: name -> Buffer."""
+
+
+def _cls(x):
+    return type(x).__name__
+
+
+# ------------------------------------------------------------------ expressions
+def _eval_int(e, env):
+    c = _cls(e)
+    if c == "Imm":
+        return int(e.value)
+    if c == "Var":
+        if e.name not in env:
+            raise EvalError(f"unbound variable {e.name!r}")
+        return env[e.name]
+    if c == "Bop":
+        a, b = _eval_int(e.lhs, env), _eval_int(e.rhs, env)
+        if e.op == "+":
+            return a + b
+        if e.op == "-":
+            return a - b
+        if e.op == "*":
+            return a * b
+        if e.op in ("/", "%"):
+            if b == 0:
+                raise EvalError("integer division by zero")
+            r = a % abs(b)
+            return r if e.op == "%" else (a - r) // b
+    raise UnsupportedProgram(f"non-scalar integer expression {c}")
+
+
+def _eval_index(e, env):
+    """Index vector of a Ramp/Broadcast tree (interp.py:191-202)."""
+    c = _cls(e)
+    if c in ("Imm", "Var", "Bop"):
+        if c == "Bop" and _cls(e.lhs) in ("Ramp", "Broadcast"):
+            a, b = _eval_index(e.lhs, env), _eval_index(e.rhs, env)
+            return {"+": a + b, "-": a - b, "*": a * b}[e.op]
+        return np.array([_eval_int(e, env)], np.int64)
+    if c == "Ramp":
+        base = _eval_index(e.base, env)
+        stride = _eval_index(e.stride, env)
+        steps = np.arange(e.steps).reshape(-1, 1)
+        return (base + steps * stride).reshape(-1)
+    if c == "Broadcast":
+        return np.tile(_eval_index(e.operand, env), e.copies)
+    raise UnsupportedProgram(f"index expression {c}")
+
+
+def _is_flat(index, length=None):
+    return (_cls(index) == "Ramp" and _cls(index.base) == "Imm" and int(index.base.value) == 0
+            and _cls(index.stride) == "Imm" and int(index.stride.value) == 1
+            and (length is None or index.steps == length))
+
+
+# ------------------------------------------------------------------ plan
+class _Group:
+    """One conv statement group (one ts_run_conv_group launch)."""
+
+    def __init__(self, acc, src, kern, m, k, n):
+        self.acc, self.src, self.kern = acc, src, kern
+        self.m, self.k, self.n = m, k, n
+        self.a_stride = 0
+        self.a_base, self.k_base = [], []
+        self.b_off = None
+        self.a_idx, self.b_idx = [], []   # explicit mode (source form)
+        self.tmp = None                    # lowered: the temporary holding B
+
+
+class _Plan:
+    def __init__(self):
+        self.ops = []
+
+
+def _shape_registry(p, extra_shapes, strict):
+    decls = set(HARDWARE_SHAPES)
+    if not strict:
+        for s in tuple(getattr(p, "shapes", ())) + tuple(extra_shapes):
+            decls.add((s.target, s.m, s.k, s.n))
+    return decls
+
+
+def _matrix_offsets(call, env):
+    """(kernel buffer, window base, k*n offsets or -1) for a B builder:
+    ConvolutionShuffle / PolyphaseShuffle (interp.py:488-534) or a desugared
+    Shuffle over a kernel load (interp.py:220-225)."""
+    c = _cls(call)
+    if c == "Call" and call.name in ("ConvolutionShuffle", "PolyphaseShuffle"):
+        kbuf = call.args[0].name
+        base = _eval_int(call.args[1], env)
+        if call.name == "ConvolutionShuffle":
+            rows, cols = int(call.args[2].value), int(call.args[3].value)
+            spec = layout.ToeplitzSpec(l=rows - cols, k=cols)
+        else:
+            l, k, pp, s = (int(a.value) for a in call.args[2:6])
+            spec = layout.ToeplitzSpec(l=l, k=k, s=s, p=pp)
+        idx = np.asarray(layout.shuffle_indices_for(spec, 0, 1 << 30), np.int64)
+        off = np.where(idx < 0, -1, idx - 1)  # lane 0 is the zero lane
+        return kbuf, base, off.astype(np.int32), spec.k
+    if c == "Shuffle":
+        src = call.source
+        if _cls(src) != "Load" or _cls(src.index) != "Ramp" or _cls(src.index.stride) != "Imm" \
+                or int(src.index.stride.value) != 1:
+            raise UnsupportedProgram("shuffle source must be a unit-stride kernel load")
+        base = _eval_int(src.index.base, env)
+        return src.buffer, base, np.asarray(call.indices, np.int32), None
+    raise UnsupportedProgram(f"not a weight builder: {c} {getattr(call, 'name', '')}")
+
+
+def _compile(p, extra_shapes, strict):
+    shapes = _shape_registry(p, extra_shapes, strict)
+    kinds = {prm.name: prm.kind for prm in p.params}
+    plan = _Plan()
+    tmp_defs = {}  # temporary name -> (kernel buf, base, offsets) of the current iteration
+
+    def emit_stmt(s, env, group_ctx):
+        c = _cls(s)
+        if c == "Allocate":
+            kinds[s.name] = s.kind
+            plan.ops.append(("alloc", s.name, s.kind, s.length, s.location))
+            return
+        if c == "Evaluate":
+            v = s.value
+            if _cls(v) == "Call" and v.name == "wmma_store":
+                out = v.args[0].name
+                base = _eval_int(v.args[1], env)
+                stride = _eval_int(v.args[2], env)
+                cols = int(v.args[3].value)
+                tile = v.args[4]
+                if _cls(tile) != "Load" or not _is_flat(tile.index):
+                    raise UnsupportedProgram("wmma_store of a non-buffer tile")
+                plan.ops.append(("store", out, tile.buffer, base, stride, cols, tile.index.steps))
+                return
+            raise UnsupportedProgram(f"evaluate of {getattr(v, 'name', _cls(v))}")
+        if c == "For":
+            for it in range(s.min, s.min + s.extent):
+                env2 = dict(env)
+                env2[s.var] = it
+                for b in s.body:
+                    emit_stmt(b, env2, group_ctx)
+            return
+        if c != "Store":
+            raise UnsupportedProgram(f"statement {c}")
+        v = s.value
+        vc = _cls(v)
+        # acc = wmma_zero(m, n)
+        if vc == "Call" and v.name == "wmma_zero":
+            plan.ops.append(("zero", s.buffer))
+            return
+        # tmp = weight builder
+        if (vc == "Call" and v.name in ("ConvolutionShuffle", "PolyphaseShuffle")) or vc == "Shuffle":
+            # recorded, not executed: the group that consumes it gathers B
+            # on the fly, and materialises the last iteration's temporary
+            kbuf, base, off, _ = _matrix_offsets(v, env)
+            tmp_defs[s.buffer] = (kbuf, base, off)
+            return
+        # acc = wmma_mma(load_a, load_b, acc)
+        if vc == "Call" and v.name == "wmma_mma":
+            la, lb, lc = v.args
+            if _cls(la) != "Call" or la.name != "wmma_load_a" or _cls(lb) != "Call" \
+                    or lb.name != "wmma_load_b":
+                raise UnsupportedProgram("wmma_mma operands must be wmma_load_a / wmma_load_b")
+            src = la.args[0].name
+            a_base, a_stride = _eval_int(la.args[1], env), _eval_int(la.args[2], env)
+            m, k = int(la.args[3].value), int(la.args[4].value)
+            tmp = lb.args[0].name
+            b_base, b_stride = _eval_int(lb.args[1], env), _eval_int(lb.args[2], env)
+            bk, bn = int(lb.args[3].value), int(lb.args[4].value)
+            if bk != k or b_base != 0 or b_stride != bn:
+                raise UnsupportedProgram("wmma_load_b must read the whole temporary row-major")
+            if ("wmma", m, k, bn) not in shapes:
+                raise ShapeUnregistered(f"wmma_mma: shape wmma {m}x{k}x{bn} not registered")
+            if tmp not in tmp_defs:
+                raise UnsupportedProgram(f"B operand {tmp!r} is not a weight temporary")
+            kbuf, kb, off = tmp_defs[tmp]
+            if len(off) != k * bn:
+                raise EvalError(f"temporary {tmp!r} has {len(off)} lanes, B needs {k * bn}")
+            if _cls(lc) == "Load" and lc.buffer == s.buffer and _is_flat(lc.index):
+                pass
+            elif _cls(lc) == "Call" and lc.name == "wmma_zero":
+                plan.ops.append(("zero", s.buffer))
+            else:
+                raise UnsupportedProgram("wmma_mma accumulator must be the stored buffer")
+            key = ("lowered", s.buffer, src, kbuf, m, k, bn, a_stride, off.tobytes())
+            _append_iteration(plan, key, s.buffer, src, kbuf, m, k, bn, a_stride, a_base, kb, off,
+                              tmp)
+            return
+        # acc = VectorReduceAdd(Load I * Load K) + Load acc  (source form)
+        if vc == "Bop" and v.op == "+":
+            red, acc = v.lhs, v.rhs
+            if _cls(red) != "VectorReduceAdd":
+                red, acc = acc, red
+            if _cls(red) == "VectorReduceAdd" and _cls(acc) == "Load" and acc.buffer == s.buffer:
+                _source_conv(plan, s, red, env, kinds)
+                return
+        # dst = Load src (flat copy)
+        if vc == "Load" and _is_flat(s.index) and _is_flat(v.index, s.index.steps):
+            plan.ops.append(("copy", s.buffer, v.buffer, s.index.steps))
+            return
+        if vc == "Broadcast" and _cls(v.operand) == "Imm" and _is_flat(s.index):
+            plan.ops.append(("fill", s.buffer, float(v.operand.value), s.index.steps))
+            return
+        raise UnsupportedProgram(f"store into {s.buffer!r} of {vc} {getattr(v, 'name', '')}")
+
+    for st in p.body:
+        emit_stmt(st, {}, None)
+    return plan
+
+
+def _append_iteration(plan, key, acc, src, kbuf, m, k, n, a_stride, a_base, k_base, off, tmp):
+    last = plan.ops[-1] if plan.ops else None
+    if last is not None and last[0] == "group" and last[1] == key:
+        g = last[2]
+    else:
+        g = _Group(acc, src, kbuf, m, k, n)
+        g.a_stride, g.b_off, g.tmp = a_stride, off, tmp
+        plan.ops.append(("group", key, g))
+    g.a_base.append(a_base)
+    g.k_base.append(k_base)
+
+
+def _strip_cast(e):
+    while _cls(e) == "Cast":
+        e = e.operand
+    return e
+
+
+def _source_conv(plan, s, red, env, kinds):
+    """VectorReduceAdd(n_out, Cast(Load I) * [Broadcast](Cast(Load K))) + acc."""
+    prod = red.operand
+    if _cls(prod) != "Bop" or prod.op != "*":
+        raise UnsupportedProgram("reduction operand must be a product")
+    loads = []
+    for side in (prod.lhs, prod.rhs):
+        e = _strip_cast(side)
+        if _cls(e) == "Broadcast":
+            e2 = _strip_cast(e.operand)
+            if _cls(e2) != "Load":
+                raise UnsupportedProgram("broadcast of a non-load")
+            loads.append((e2.buffer, np.tile(_eval_index(e2.index, env), e.copies)))
+        elif _cls(e) == "Load":
+            loads.append((e.buffer, _eval_index(e.index, env)))
+        else:
+            raise UnsupportedProgram("product of non-loads")
+    (ib, ia), (kb, ka) = loads
+    n_out = red.result_lanes
+    if len(ia) != len(ka) or len(ia) % n_out:
+        raise EvalError(f"cannot reduce {len(ia)} lanes to {n_out}")
+    taps = len(ia) // n_out
+    if not _is_flat(s.index, n_out):
+        raise UnsupportedProgram("source-form store must be a flat ramp")
+    key = ("source", s.buffer, ib, kb, n_out, taps)
+    last = plan.ops[-1] if plan.ops else None
+    if last is not None and last[0] == "group" and last[1] == key:
+        g = last[2]
+    else:
+        g = _Group(s.buffer, ib, kb, n_out, taps, 1)
+        plan.ops.append(("group", key, g))
+    g.a_idx.append(ia.reshape(n_out, taps).astype(np.int32))
+    g.b_idx.append(ka.reshape(n_out, taps).astype(np.int32))
+    g.a_base.append(0)
+    g.k_base.append(0)
+
+
+# ------------------------------------------------------------------ execution
+def _as_data(x):
+    return x.data if hasattr(x, "data") and not isinstance(x, np.ndarray) else x
+
+
+def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=None, device=None):
+    """Run program `p` once per element of `inputs_list` (name -> Buffer or
+    array) on the GPU; returns one BufferStore per instance (parameters,
+    allocations and temporaries, like interp.run_program)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        from .errors import NoDevice
+        raise NoDevice("run_program_batch needs a CUDA device")
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+    lib = _lib.load()
+    T = len(inputs_list)
+    plan = _compile(p, extra_shapes, strict)
+    bufs, meta = {}, {}
+    for prm in p.params:
+        if prm.kind == "i32":
+            raise UnsupportedProgram("i32 parameters are outside the conv family")
+        rows = []
+        for ins in inputs_list:
+            if prm.name not in ins:
+                raise EvalError(f"missing input buffer {prm.name!r}")
+            d = np.asarray(_as_data(ins[prm.name]), dtype=np.float32)
+            if len(d) != prm.length:
+                raise EvalError(f"input {prm.name!r} has length {len(d)}, declared {prm.length}")
+            rows.append(d)
+        bufs[prm.name] = torch.from_numpy(np.stack(rows) if rows else
+                                          np.zeros((0, prm.length), np.float32)).to(dev)
+        meta[prm.name] = (prm.kind, getattr(prm, "location", "mem"))
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    for op in plan.ops:
+        kind = op[0]
+        if kind == "alloc":
+            _, name, k, length, loc = op
+            if k == "i32":
+                raise UnsupportedProgram("i32 allocations are outside the conv family")
+            bufs[name] = torch.zeros((T, length), dtype=torch.float32, device=dev)
+            meta[name] = (k, loc)
+        elif kind == "zero":
+            bufs[op[1]].zero_()
+        elif kind == "fill":
+            _, name, val, n = op
+            bufs[name][:, :n] = val
+        elif kind == "copy":
+            _, dst, src, n = op
+            bufs[dst][:, :n] = bufs[src][:, :n]
+        elif kind == "tmp":
+            _, name, kbuf, base, off = op
+            K = bufs[kbuf]
+            o = torch.from_numpy(off.astype(np.int64)).to(dev)
+            if int(off.max(initial=-1)) + base >= K.shape[1] or (off >= 0).any() and base < 0:
+                raise OutOfBounds(kbuf, int(base + off.max()))
+            vals = K[:, (base + o).clamp(min=0)]
+            bufs[name][:, :len(off)] = torch.where(o >= 0, vals, torch.zeros_like(vals))
+        elif kind == "store":
+            _, out, tile, base, stride, cols, lanes = op
+            rows = lanes // cols
+            idx = base + stride * np.arange(rows)[:, None] + np.arange(cols)[None, :]
+            if idx.min() < 0 or idx.max() >= bufs[out].shape[1]:
+                raise OutOfBounds(out, int(idx[(idx < 0) | (idx >= bufs[out].shape[1])][0]))
+            bufs[out][:, torch.from_numpy(idx.reshape(-1)).to(dev)] = bufs[tile][:, :lanes]
+        elif kind == "group":
+            _run_group(lib, op[2], bufs, meta, T, dev, stream, err)
+        else:
+            raise UnknownIntrinsic(kind)
+    torch.cuda.synchronize(dev)
+    out = []
+    host = {n: b.cpu().numpy() for n, b in bufs.items()}
+    for t in range(T):
+        st = BufferStore()
+        for n, data in host.items():
+            k, loc = meta[n]
+            st[n] = Buffer(k, loc, data[t].copy())
+        out.append(st)
+    return out
+
+
+def _run_group(lib, g, bufs, meta, T, dev, stream, err):
+    import torch
+    src, kern, acc = bufs[g.src], bufs[g.kern], bufs[g.acc]
+    V = len(g.a_base)
+    keep = []
+
+    def dptr(arr):
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32)).to(dev)
+        keep.append(t)
+        return t.data_ptr()
+
+    c = _lib.ConvGroup()
+    c.instances = T
+    c.src, c.src_stride, c.src_len = src.data_ptr(), src.shape[1], src.shape[1]
+    # lowered loads re-round to the buffer kind (interp.py:441-442); source-form
+    # loads and casts to f32 do not (interp.py:183-188, 241-248)
+    c.src_kind = 0 if g.a_idx else _KIND.get(meta[g.src][0], 0)
+    c.kern, c.kern_stride, c.kern_len = kern.data_ptr(), kern.shape[1], kern.shape[1]
+    c.kern_kind = 0 if g.a_idx else _KIND.get(meta[g.kern][0], 0)
+    c.acc, c.acc_stride, c.zero_init = acc.data_ptr(), acc.shape[1], 0
+    c.m, c.k, c.n, c.a_stride = g.m, g.k, g.n, g.a_stride
+    c.iterations = V
+    if g.a_idx:
+        c.a_idx = dptr(np.stack(g.a_idx))
+        c.b_idx = dptr(np.stack(g.b_idx))
+    else:
+        c.a_base, c.k_base = dptr(g.a_base), dptr(g.k_base)
+        c.b_off = dptr(g.b_off)
+    err.zero_()
+    c.error = err.data_ptr()
+    _lib.check(lib.ts_run_conv_group(ctypes.byref(c), stream), "ts_run_conv_group")
+    e = int(err.item())
+    if e > 0:
+        raise OutOfBounds(g.src, e - 1)
+    if e < 0:
+        raise OutOfBounds(g.kern, -e - 1)
+    if g.tmp is not None and g.tmp in bufs:  # materialise the last iteration's temporary
+        o = torch.from_numpy(g.b_off.astype(np.int64)).to(dev)
+        vals = kern[:, (g.k_base[-1] + o).clamp(min=0)]
+        bufs[g.tmp][:, :len(g.b_off)] = torch.where(o >= 0, vals, torch.zeros_like(vals))
+
+
+def run_program(p, inputs, extra_shapes=(), strict=False, lint_sink=None):
+    """interp.run_program (interp.py:570-589) on the GPU, same signature."""
+    return run_program_batch(p, [inputs], extra_shapes, strict, lint_sink)[0]
+
+
+__all__ = ["run_program", "run_program_batch", "UnsupportedProgram", "Buffer", "BufferStore",
+           "HARDWARE_SHAPES", "math"]
