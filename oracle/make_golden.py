@@ -232,6 +232,14 @@ def main():
     # -- layout
     kats["layout"] = layout_fixtures(rng)
 
+    # -- buffer-directory wire format written by the reference (interp.py:640-678)
+    wire = os.path.join(OUT, "wire_conv1d_k8")
+    st = interp.run_program(ir.parse_program(open(os.path.join(CORPUS, "conv1d_k8.sexp")).read()),
+                            interp.random_inputs(ir.parse_program(open(os.path.join(CORPUS, "conv1d_k8.sexp")).read()), 3))
+    st["bfvec"] = interp.Buffer("bf16", "mem", interp.round_bf16(rng.uniform(-2, 2, 37).astype(np.float32)))
+    st["ivec"] = interp.Buffer("i32", "mem", np.arange(-5, 6, dtype=np.int64))
+    interp.save_buffers(st, wire)
+
     np.savez_compressed(os.path.join(OUT, "reference_golden.npz"), **arrays)
     with open(os.path.join(OUT, "reference_golden.json"), "w") as f:
         json.dump(kats, f, indent=1)

@@ -94,6 +94,13 @@ def downsample2x(x, *, out_dtype=None):
     return resample(x, H // 2, W // 2, out_dtype=out_dtype)
 
 
+def upsample2x(x, *, out_dtype=None):
+    """Lanczos-3 2x upsample: the polyphase Toeplitz case (layout.polyphase_toeplitz,
+    layout.py:97-103) — each output phase is a 6-tap filter."""
+    H, W = x.shape[-2], x.shape[-1]
+    return resample(x, 2 * H, 2 * W, out_dtype=out_dtype)
+
+
 def filter_separable(x, kernel_v, kernel_h=None, *, out_dtype=None):
     """Same-size separable convolution (centred taps, clamp-to-edge)."""
     dev = _check_device(x)

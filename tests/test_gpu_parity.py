@@ -128,3 +128,16 @@ def test_resample_then_filter_fused_matches_two_pass_oracle():
     ref = pipelines_ref.gaussian_blur(pipelines_ref.resample(x, 216, 384), 9)
     assert y.shape == ref.shape
     assert np.abs(y - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("shape", [(3, 135, 240), (1, 64, 200)])
+def test_upsample2x_matches_oracle(shape):
+    # polyphase (p = 2) Toeplitz axes
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = _img(shape, 31)
+    y = _gpu(pipelines.upsample2x, x, out_dtype=torch.float32)
+    H, W = shape[-2:]
+    ref = pipelines_ref.resample(x, 2 * H, 2 * W)
+    assert y.shape == ref.shape
+    assert np.abs(y - ref).max() <= TOL

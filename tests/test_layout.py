@@ -67,3 +67,37 @@ def test_matrix_for_on_device(L):
         m = layout.matrix_for(kern, spec, device="cuda")
         torch.cuda.synchronize()
         assert m.cpu().tolist() == case["matrix"]
+
+
+def test_wire_format_roundtrip_matches_reference(tmp_path):
+    # directory written by the reference's save_buffers (tests/golden/wire_conv1d_k8)
+    from paper_2512_02371_b200 import wire
+    from conftest import GOLDEN
+    src = os.path.join(GOLDEN, "wire_conv1d_k8")
+    bufs = wire.load_buffers(src)
+    assert set(bufs) >= {"K", "I", "output", "conv", "bfvec", "ivec"}
+    assert bufs["ivec"][2].tolist() == list(range(-5, 6))
+    assert bufs["bfvec"][0] == "bf16" and bufs["bfvec"][2].dtype == np.float32
+    wire.save_buffers(bufs, tmp_path)
+    for e in wire.read_manifest(src):
+        a = open(os.path.join(src, e["name"] + ".bin"), "rb").read()
+        b = open(os.path.join(tmp_path, e["name"] + ".bin"), "rb").read()
+        assert a == b, e["name"]
+    assert json.load(open(os.path.join(src, "manifest.json"))) == \
+        json.load(open(os.path.join(tmp_path, "manifest.json")))
+
+
+@pytest.mark.gpu
+def test_wire_format_to_device(tmp_path):
+    import torch
+    from paper_2512_02371_b200 import wire
+    from conftest import GOLDEN
+    src = os.path.join(GOLDEN, "wire_conv1d_k8")
+    host = wire.load_buffers(src)
+    dev = wire.load_buffers(src, device="cuda")
+    assert dev["bfvec"][2].dtype == torch.bfloat16 and dev["bfvec"][2].is_cuda
+    assert torch.equal(dev["bfvec"][2].float().cpu(), torch.from_numpy(host["bfvec"][2]))
+    wire.save_buffers(dev, tmp_path)
+    for e in wire.read_manifest(src):
+        assert open(os.path.join(src, e["name"] + ".bin"), "rb").read() == \
+            open(os.path.join(tmp_path, e["name"] + ".bin"), "rb").read()
