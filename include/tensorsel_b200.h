@@ -126,6 +126,20 @@ TS_API ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int 
 TS_API ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes,
                                    int out_dtype, int* out8);
 
+/* Which kernel ts_separable_run launches for these axes: 5 = strip kernel
+ * (Toeplitz-like axes: uniform 16-output block spacing of 8/16/32 inputs;
+ * the banded weights become one shifted strip per axis), 4 = block-tile
+ * kernel (any banded axes).  The strip kernel is opt-in: only with the
+ * environment variable TSB_STRIP=1 (it is slower than 4 on B200 today). */
+TS_API int ts_separable_variant(const ts_axis* rows, const ts_axis* cols, int planes, int out_dtype);
+
+/* Diagnostics: geometry of the last strip-kernel launch or variant query:
+ * out16 = {valid, ring slots, K-steps rows, K-steps cols, output columns per
+ * tile, staged columns, pass-1 N, edge slices rows, edge slices cols, work
+ * units, row tiles per unit, smem bytes, V separate, D_H double, chunk
+ * bytes, row tiles}.  Returns out16[0]. */
+TS_API int ts_strip_info(int* out16);
+
 /* Fused DCT-16 transform-domain denoise: 16x16 tiles at
  * stride 8, sine window folded into the DCT-II matrices, coring of every
  * non-DC coefficient (soft = 0: |c| < threshold -> 0; soft = 1: shrink by
@@ -224,6 +238,15 @@ TS_API ts_status ts_probe_issue(int variant, long long* cycles, void* stream);
 /* Same with A read from TMEM (TS mode); variant 0..3 = (N, kind) in
  * {(16, f16), (64, f16), (16, tf32), (64, tf32)}. */
 TS_API ts_status ts_probe_issue_ts(int variant, long long* cycles, void* stream);
+/* Streaming-operand issue rate: `count` elected M=128, K=16 MMAs cycling over
+ * 8 K-slices; amode 0 smem MN-major SW128 / 1 smem K-major / 2 TMEM,
+ * bmode 0 smem K-major / 1 smem MN-major SW128; nacc accumulators. */
+/* TMA streaming probe: grid CTAs stream a planes x H x W bf16 tensor in
+ * chunks of rows x (64 * nbox) through an nr-slot ring (load path only). */
+TS_API ts_status ts_probe_tma(const void* src, int planes, int H, int W, int rows, int nbox, int nr,
+                              int grid, void* stream);
+TS_API ts_status ts_probe_issue2(int amode, int bmode, int n, int count, int nacc,
+                                 long long* cycles, void* stream);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,10 @@ _SIGNATURES = {
     "ts_axis_destroy": (None, [_P]),
     "ts_separable_run": (_I, [_P, _P, _I, _P, _I64, _I64, _I, _P, _I64, _I64, _I, _P]),
     "ts_separable_plan": (_I, [_P, _P, _I, _I, ctypes.POINTER(ctypes.c_int)]),
+    "ts_separable_variant": (_I, [_P, _P, _I, _I]),
+    "ts_strip_info": (_I, [ctypes.POINTER(ctypes.c_int)]),
+    "ts_probe_tma": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P]),
+    "ts_probe_issue2": (_I, [_I, _I, _I, _I, _I, _P, _P]),
     "ts_cast_f32_bf16": (_I, [_P, _P, _I64, _P]),
     "ts_run_conv_group": (_I, [_P, _P]),
     "ts_debug_dct16": (_I, [_P]),

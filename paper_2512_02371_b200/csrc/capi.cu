@@ -16,6 +16,8 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
 ts_status separable_plan(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype,
                          int* out8);
 void set_trace(void* buf, int ctas, int tiles);
+int separable_variant(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype);
+int strip_info(int* out16);
 
 // ------------------------------------------------------------------ cast
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -160,6 +162,12 @@ ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes
                             int* out8) {
   return separable_plan(rows, cols, planes, out_dtype, out8);
 }
+
+int ts_separable_variant(const ts_axis* rows, const ts_axis* cols, int planes, int out_dtype) {
+  return separable_variant(rows, cols, planes, out_dtype);
+}
+
+int ts_strip_info(int* out16) { return out16 ? strip_info(out16) : 0; }
 
 ts_status ts_debug_trace(void* device_buffer, int ctas, int tiles) {
   if (device_buffer && (ctas < 1 || tiles < 1))

@@ -35,6 +35,31 @@ struct AxisDev {
 
 }  // namespace tsb
 
+namespace tsb {
+// Shift-invariant "strip" form of an axis for the v5 separable kernel
+// (csrc/strip.cpp): per tile, K-step q's operand slice equals a fixed strip
+// shifted by `shift` outputs per 16 inputs, except a few edge slices.
+struct StripPlan {
+  bool ok = false;
+  const char* why = "";
+  int role = 0;             // 0 rows (pass-1 A), 1 cols (pass-2 B)
+  int S = 0;                // input spacing between 16-output blocks
+  int shift = 0;            // outputs moved per 16-input K-step (multiple of 8)
+  int Q = 0;                // K-steps per tile
+  int G = 0;                // 8-output groups stored above output 0 in the strip
+  int nout = 0;             // outputs per tile (128 rows / NO cols)
+  int ntiles = 0;           // tiles along the axis
+  int staged = 0;           // cols role: input columns staged per tile (multiple of 64)
+  std::vector<int32_t> first_in;   // per tile: first input index of its window
+  std::vector<uint16_t> strip;     // (nout + 8G) x 16 bf16, K-major core matrices
+  std::vector<uint16_t> specials;  // nspec x (nout x 16) bf16, same layout
+  std::vector<int8_t> map;         // ntiles x Q: -1 strip, else special index
+  int nspec = 0;
+  uint8_t* d_strip = nullptr;
+  uint8_t* d_specials = nullptr;
+};
+}  // namespace tsb
+
 struct ts_axis {
   int n_in = 0, n_out = 0, taps = 0;
   int K = 0, nb = 0, ntiles = 0, tile_bytes = 0;
@@ -48,6 +73,7 @@ struct ts_axis {
   int32_t* d_tab = nullptr;
   uint8_t* d_tiles = nullptr;
   std::vector<int32_t> tab;         // packed (ws << 16) | tid, nb + kBlockPad entries
+  mutable tsb::StripPlan* strip[2] = {nullptr, nullptr};  // lazily built per role
 
   tsb::AxisDev dev() const {
     return tsb::AxisDev{d_ws, d_tid, d_tab, d_tiles, K, nb, tile_bytes, ntiles};

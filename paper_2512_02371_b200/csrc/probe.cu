@@ -44,8 +44,8 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t raw_s = smem_u32(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_s - raw_s);
-  const bool tf32 = amode >= 2;
-  const bool a_tmem = amode == 2;
+  const bool tf32 = amode >= 2 && amode <= 4;
+  const bool a_tmem = amode == 2 || amode == 5;
   const int es = tf32 ? 4 : 2;
   const uint32_t a_bytes = a_tmem ? 0u : 128u * k * (tf32 ? 4u : 2u);
   const uint32_t b_bytes = static_cast<uint32_t>(k) * n * es;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128, 1)
       *reinterpret_cast<float*>(sa + off) = a[e];
     }
   }
-  if (!tf32) {
+  if (!tf32 && !a_tmem) {
     for (int e = threadIdx.x; e < 128 * k; e += blockDim.x) {
       const int m = e / k, kk = e % k;
       uint32_t off;
@@ -113,7 +113,21 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tmem = *slot;
   const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
 
-  if (a_tmem) {
+  if (a_tmem && amode == 5) {
+    // A row m = lane m; packed bf16 pairs: column c holds (k = 2c, 2c + 1)
+    const int m = warp * 32 + lane;
+    for (int c0 = 0; c0 < k / 2; c0 += 16) {
+      uint32_t r[16];
+      for (int i = 0; i < 16; ++i)
+        r[i] = (c0 + i) * 2 < k ? pack_bf16x2(a[m * k + 2 * (c0 + i)], a[m * k + 2 * (c0 + i) + 1])
+                                : 0u;
+      tmem_st16(lane_base + 256u + c0, r);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  } else if (a_tmem) {
     // A row m = this thread's TMEM lane, columns [256, 256 + k)
     const int m = warp * 32 + lane;
     for (int c0 = 0; c0 < k; c0 += 16) {
@@ -132,7 +146,7 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t idesc =
         make_idesc(tf32 ? kFmtTF32 : kFmtBF16, 128, n, (amode == 0 || amode == 3) ? 1u : 0u,
                    bmode == 1 ? 1u : 0u);
-    const int kstep = tf32 ? 8 : 16;
+    const int kstep = tf32 ? 8 : 16;  // amode 5 (f16 TS) uses K = 16
     t0 = clock64();
     for (int r = 0; r < reps; ++r) {
       // nacc > 1: round-robin the repetitions over nacc accumulators (columns
@@ -140,7 +154,14 @@ __global__ void __launch_bounds__(128, 1)
       const uint32_t dcol = static_cast<uint32_t>((r % nacc) * n);
       for (int q = 0; q < k / kstep; ++q) {
         const uint32_t acc = (r >= nacc || q > 0) ? 1u : 0u;
-        if (tf32) {
+        if (amode == 5) {
+          const uint64_t bd = make_sdesc(base_s + a_bytes + q * 256u, 128u, k * 16u, kSwizzleNone);
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + dcol),
+              "r"(tmem + 256u + q * 8u), "l"(bd), "r"(idesc), "r"(acc)
+              : "memory");
+        } else if (tf32) {
           const uint64_t bd = make_sdesc(base_s + a_bytes + q * 256u, 128u,
                                          static_cast<uint32_t>(k / 4) * 128u, kSwizzleNone);
           if (amode == 2) {
@@ -196,13 +217,14 @@ using namespace tsb;
 extern "C" ts_status ts_probe_mma(int amode, int bmode, const float* a, const float* b, float* d,
                                   int k, int n, int reps, long long* cycles, int nacc,
                                   void* stream) {
-  const int kstep = amode >= 2 ? 8 : 16;
-  if (amode < 0 || amode > 4 || bmode < 0 || bmode > 1 || (amode >= 2 && bmode != 0) || !a ||
+  const int kstep = (amode >= 2 && amode <= 4) ? 8 : 16;
+  if (amode < 0 || amode > 5 || bmode < 0 || bmode > 1 || (amode >= 2 && bmode != 0) || !a ||
       !b || !d || k < kstep || k > 256 || k % 16 || n < 16 || n > 256 || n % 16 || reps < 1 ||
-      nacc < 1 || nacc * n > (amode == 2 ? 256 : 512) || (amode >= 3 && k > 128))
+      nacc < 1 || nacc * n > ((amode == 2 || amode == 5) ? 256 : 512) ||
+      (amode >= 3 && amode <= 4 && k > 128))
     return set_error(TS_ERR_INVALID, "probe_mma: bad arguments");
-  const int es = amode >= 2 ? 4 : 2;
-  const uint32_t a_bytes = amode == 2 ? 0u : 128u * k * (amode >= 3 ? 4u : 2u);
+  const int es = (amode >= 2 && amode <= 4) ? 4 : 2;
+  const uint32_t a_bytes = (amode == 2 || amode == 5) ? 0u : 128u * k * (amode >= 3 ? 4u : 2u);
   const uint32_t b_bytes = static_cast<uint32_t>(k) * n * es;
   const uint32_t smem = 1024 + a_bytes + ((b_bytes + 1023u) & ~1023u) + 64;
   cudaError_t e =
@@ -364,4 +386,166 @@ extern "C" ts_status ts_probe_issue_ts(int variant, long long* cycles, void* str
     default: return set_error(TS_ERR_INVALID, "probe_issue_ts: variant 0..3");
   }
   return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_issue_ts launch");
+}
+
+// Issue-rate probe with streaming operands: `count` elected MMAs, M = 128,
+// K = 16, cycling over 8 distinct K-slices of A and B (as a real K loop does).
+//   amode 0: A smem MN-major SW128   1: A smem K-major no swizzle   2: A TMEM (bf16 pairs)
+//   bmode 0: B smem K-major no swizzle   1: B smem MN-major SW128 (64-col atoms at 2048 B)
+namespace tsb {
+__global__ void __launch_bounds__(128, 1)
+    probe_issue2_kernel(int amode, int bmode, int n, int count, int nacc, long long* cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_s = smem_u32(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_s - raw_s);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 131072);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  for (int i = threadIdx.x; i < 131072 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(0x3f803f80u, 0, 0x3f803f80u, 0);
+  fence_proxy_async_smem();
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (warp == 0) {
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, n, amode == 0 ? 1u : 0u, bmode == 1 ? 1u : 0u);
+    const uint32_t b0 = base_s + 65536u;
+    const uint32_t bstep = bmode == 0 ? static_cast<uint32_t>(n) * 32u : ((n + 63) / 64) * 2048u;
+    __syncwarp();
+    const long long t0 = clock64();
+    for (int i = 0; i < count; ++i) {
+      const int q = i & 7;
+      const uint32_t d = tmem + static_cast<uint32_t>((i % nacc) * n);
+      const uint32_t acc = i >= nacc ? 1u : 0u;
+      const uint64_t bd = bmode == 0 ? make_sdesc(b0 + q * bstep, 128u, 256u, kSwizzleNone)
+                                     : make_sdesc(b0 + q * bstep, 2048u, 1024u, kSwizzle128B);
+      if (amode == 2) {
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+            "r"(tmem + 384u + q * 8u), "l"(bd), "r"(idesc), "r"(acc)
+            : "memory");
+      } else {
+        const uint64_t ad = amode == 0 ? make_sdesc(base_s + q * 2048u, 16384u, 1024u, kSwizzle128B)
+                                       : make_sdesc(base_s + q * 4096u, 128u, 256u, kSwizzleNone);
+        mma_f16_ss_elect(d, ad, bd, idesc, acc);
+      }
+    }
+    mma_commit_elect(bar);
+    mbar_wait(bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) *cycles = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+}  // namespace tsb
+
+extern "C" ts_status ts_probe_issue2(int amode, int bmode, int n, int count, int nacc,
+                                     long long* cycles, void* stream) {
+  if (amode < 0 || amode > 2 || bmode < 0 || bmode > 1 || n < 16 || n > 256 || n % 16 ||
+      nacc < 1 || n * nacc > (amode == 2 ? 384 : 512) || count < 1)
+    return set_error(TS_ERR_INVALID, "probe_issue2: bad arguments");
+  auto k = probe_issue2_kernel;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
+  if (e == cudaSuccess) {
+    k<<<1, 128, 140000, static_cast<cudaStream_t>(stream)>>>(amode, bmode, n, count, nacc, cycles);
+    e = cudaGetLastError();
+  }
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_issue2 launch");
+}
+
+// TMA streaming probe: every CTA walks column strips of a (planes x H x W)
+// bf16 tensor top to bottom in chunks of `rows` rows x (64 * nbox) columns
+// through an `nr`-slot ring; the consumer releases each chunk as soon as it
+// lands.  Measures the load path alone (boxes of 64 x rows, 128B swizzle).
+namespace tsb {
+ts_status encode_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* ptr,
+                         int64_t d0, int64_t d1, int64_t d2, int64_t stride1_elems,
+                         int64_t stride2_elems, int box0, int box1, CUtensorMapSwizzle swz);
+
+__global__ void __launch_bounds__(64, 1)
+    probe_tma_kernel(const __grid_constant__ CUtensorMap tm, int planes, int H, int W, int rows,
+                     int nbox, int nr) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_s = smem_u32(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_s - raw_s);
+  const uint32_t chunk = static_cast<uint32_t>(rows) * 128u * nbox;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + nr * chunk);
+  uint64_t* empty = full + 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nr; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int strips = (W + 64 * nbox - 1) / (64 * nbox);
+  const int chunks = (H + rows - 1) / rows;
+  const int units = planes * strips;
+  if (threadIdx.x == 0) {
+    int slot = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int p = u / strips, st = u % strips;
+      for (int c = 0; c < chunks; ++c) {
+        mbar_wait(&empty[slot], ph ^ 1);
+        mbar_arrive_expect_tx(&full[slot], chunk);
+        for (int h = 0; h < nbox; ++h)
+          tma_load_3d(base + slot * chunk + h * rows * 128, &tm, &full[slot], (st * nbox + h) * 64,
+                      c * rows, p);
+        if (++slot == nr) {
+          slot = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    int slot = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x)
+      for (int c = 0; c < chunks; ++c) {
+        mbar_wait(&full[slot], ph);
+        mbar_arrive(&empty[slot]);
+        if (++slot == nr) {
+          slot = 0;
+          ph ^= 1;
+        }
+      }
+  }
+}
+}  // namespace tsb
+
+extern "C" ts_status ts_probe_tma(const void* src, int planes, int H, int W, int rows, int nbox,
+                                  int nr, int grid, void* stream) {
+  using namespace tsb;
+  if (!src || rows < 1 || rows > 256 || nbox < 1 || nr < 1 || nr > 32 || W % 64)
+    return set_error(TS_ERR_INVALID, "probe_tma: bad arguments");
+  const uint32_t smem = static_cast<uint32_t>(nr) * rows * 128u * nbox + 1024u + 1024u;
+  if (smem > 232448) return set_error(TS_ERR_INVALID, "probe_tma: ring too large");
+  CUtensorMap tm;
+  ts_status st = encode_tmap_3d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, src, W, H, planes, W,
+                                static_cast<int64_t>(W) * H, 64, rows, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != TS_OK) return st;
+  cudaError_t e =
+      cudaFuncSetAttribute(probe_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) {
+    probe_tma_kernel<<<grid, 64, smem, static_cast<cudaStream_t>(stream)>>>(tm, planes, H, W, rows,
+                                                                            nbox, nr);
+    e = cudaGetLastError();
+  }
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_tma launch");
 }

@@ -38,6 +38,10 @@
 
 namespace tsb {
 
+ts_status strip_run(const ts_axis* ra, const ts_axis* ca, int planes, const void* in, int64_t in_rs,
+                    int64_t in_ps, void* out, int64_t out_rs, int64_t out_ps, int out_dtype,
+                    cudaStream_t stream, bool dry);
+
 constexpr int kMaxStages = 4;
 constexpr int kThreads = 352;
 constexpr uint32_t kTmemCols = 512;
@@ -551,6 +555,12 @@ static ts_status launch_sep(const SepParams& P, const CUtensorMap& tin, const CU
 static unsigned long long* g_trace = nullptr;
 static int g_trace_ctas = 0, g_trace_tiles = 0;
 
+void get_trace(unsigned long long** buf, int* ctas, int* tiles) {
+  *buf = g_trace;
+  *ctas = g_trace_ctas;
+  *tiles = g_trace_tiles;
+}
+
 void set_trace(void* buf, int ctas, int tiles) {
   g_trace = static_cast<unsigned long long*>(buf);
   g_trace_ctas = buf ? ctas : 0;
@@ -612,6 +622,11 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   cudaError_t de = cudaSetDevice(ra->device);
   if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
 
+  // Toeplitz-like axes take the strip kernel (separable_strip.cu)
+  ts_status s5 = strip_run(ra, ca, planes, in, in_rs, in_ps, out, out_rs, out_ps, out_dtype,
+                           stream, false);
+  if (s5 != TS_ERR_UNSUPPORTED) return s5;
+
   SepParams P;
   ts_status st = make_params(ra, ca, planes, oes, P);
   if (st != TS_OK) return st;
@@ -627,6 +642,15 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   if (st != TS_OK) return st;
   if (out_dtype == TS_BF16) return launch_sep<__nv_bfloat16>(P, tin, tout, stream);
   return launch_sep<float>(P, tin, tout, stream);
+}
+
+// Which kernel ts_separable_run would launch: 5 (strip) or 4 (block tiles).
+int separable_variant(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype) {
+  if (!ra || !ca) return -TS_ERR_INVALID;
+  int64_t rs = (ca->n_in + 7) / 8 * 8, ors = (ca->n_out + 7) / 8 * 8;
+  ts_status s5 = strip_run(ra, ca, planes < 1 ? 1 : planes, nullptr, rs, rs * ra->n_in, nullptr,
+                           ors, ors * ra->n_out, out_dtype, nullptr, true);
+  return s5 == TS_OK ? 5 : 4;
 }
 
 // The launch geometry a run would use (ts_separable_plan).
