@@ -6,25 +6,30 @@
 // domain (hard or soft threshold; DC kept), clamp-to-edge outside the image.
 //
 // One persistent CTA per SM; work unit = a 128x128 input band at image
-// offset (Y-8, X-8) producing the 112x112 output block (Y.., X..).  The 16x16
-// tiles of the band split into row phases p (tile rows at band row 8p+16i)
-// and column phases q (8q+16j); for each p the kernel runs four tcgen05
-// steps (M=128, N=16), choosing operand majors so no explicit transposes are
-// needed:
-//   S1 (SS, bf16)  D1[c][16i+k]   = Σ_r X[16i+8p+r][c] Dw[k][r]    A = band, MN-major
-//   E1             D1 -> S_Y (bf16 hi + lo pair, MN-major: M = freq-row m, K = col)
-//   S3 (SS, bf16)  D2[m][16(8q+j)+l] = Σ_c (Y_hi + Y_lo)[m][16j+8q+c] Dw[l][c]
-//   E2             coring of D2 in TMEM (in place)
-//   S5 (TS, tf32)  D3[m][16j+8q+c] += Σ_l C'[m][..+l] Dw[l][c]     A = D2 from TMEM
-//   E3             D3 -> S_R (bf16 hi + lo, MN-major: M = col, K = freq-row)
-//   S7 (SS, bf16)  D4[c][16i+8p+r] += Σ_k (R_hi + R_lo)[16i+k][c] Dw[k][r]  (both p accumulate)
-// (kind::tf32 does not accept an MN-major A from shared memory on sm_100a —
-// it silently yields zeros, see ts_probe_mma amode 3 — so f32 intermediates
-// travel as bf16 hi/lo pairs, two MMAs per K step, ~16 mantissa bits.)
-// and finally E4: D4 (lane = column, columns = band rows) -> bf16/f32 -> TMA
-// store of the 112x112 block.  Steps run in sequence within a CTA (MMA warp
-// and epilogue warpgroup hand off through mbarriers); the next band's TMA
-// load overlaps the current band.
+// offset (Y-8, X-8) producing the 112x112 output block (Y.., X..).  The
+// 16x16 tiles of the band split into row phases p (tiles at band rows
+// 16i+8p) and column phases q (band columns 16j+8q).  Per row phase, with
+// f = 16i + k the (tile row, row frequency) index — the TMEM lane:
+//
+//   S1  (SS bf16, N=128)  D1[f][c]  = Σ_r T_p[f][r] X[r][c]
+//         A = T_p, the block-banded forward column transform (a shifted
+//         strip, hi + lo), B = the band straight from TMA (MN-major)
+//   C1  D1 -> bf16 hi/lo pairs, in TMEM (no shared-memory round trip)
+//   S3  (TS bf16, N=16)   D2[f][16(8q+j)+l] = Σ_c D1[f][16j+8q+c] Dw[l][c]
+//         (hi·hi + lo·hi + hi·lo), A read from TMEM
+//   E2  coring of D2 in place (DC kept)
+//   S5  (TS tf32, N=16)   D3[f][16j+8q+c] (+)= Σ_l D2'[f][..+l] Dw[l][c]
+//   E3  D3 -> B7 (bf16 hi/lo, MN-major: K = f, N = c) in shared memory
+//   S7  (SS bf16, N=128)  D4[r][c] += Σ_f T_pᵀ[r][f] B7[f][c]   (both p accumulate)
+//   E4  D4 (lane = band row) -> output block, one TMA store
+//
+// Clamp-to-edge: TMA zero-fills samples outside the image; for bands on an
+// image border the loader warp replicates the edge row / column into the 8
+// samples beyond it inside the staged band (equivalent to folding the
+// outside weights onto the edge sample), so the transforms have no edge
+// variants.  (kind::tf32 does not accept an MN-major A from shared memory on
+// sm_100a — it silently yields zeros, see ts_probe_mma amode 3 — so f32
+// intermediates travel as bf16 hi/lo pairs, ~16 mantissa bits.)
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -41,40 +46,57 @@ ts_status encode_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, cons
                          int64_t d0, int64_t d1, int64_t d2, int64_t stride1_elems,
                          int64_t stride2_elems, int box0, int box1, CUtensorMapSwizzle swz);
 int sm_count_current();
+void get_trace(unsigned long long** buf, int* ctas, int* tiles);
 
 namespace dct {
 
-constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kEpiThreads = 512;                 // warps 2-17: epilogue
+constexpr int kThreads = 64 + kEpiThreads;    // warp 0 loader, warp 1 MMA
 constexpr int kBand = 128;
 constexpr int kOut = 112;
 constexpr uint32_t kBandBytes = kBand * kBand * 2;  // bf16 band, two 64-col SW128 halves
-constexpr uint32_t kOpBytes = 128 * 128 * 4;        // bf16 hi + lo operand (S_Y / S_R alias)
-constexpr uint32_t kOpLo = 128 * 128 * 2;           // offset of the lo half
 
 // smem layout (bytes from the 1024-aligned base)
-constexpr uint32_t kOffX = 0;                           // 2 band buffers
-constexpr uint32_t kOffOp = kOffX + 2 * kBandBytes;     // S_Y / S_R
-constexpr uint32_t kOffOut = kOffOp + kOpBytes;         // 112 x 112 staging (f32 worst case)
+constexpr uint32_t kOffX = 0;                            // 2 band buffers
+constexpr uint32_t kOffB7 = kOffX + 2 * kBandBytes;      // S7 B operand: hi, lo (32 KB each)
+constexpr uint32_t kB7Lo = 32768;
+constexpr uint32_t kOffOut = kOffB7 + 2 * 32768;         // 112 x 112 staging (f32 worst case)
 constexpr uint32_t kOutBytes = kOut * kOut * 4;
-constexpr uint32_t kOffB = kOffOut + ((kOutBytes + 1023) / 1024) * 1024;
-// constant B tiles: bf16 Dwᵀ hi + lo (S1, S3: the steps whose rounding decides
-// which coefficients are cored) in three edge variants each — 0 interior,
-// 1 "low cut" (samples 0..7 lie outside the image: their weight is folded
-// onto sample 8, clamp-to-edge), 2 "high cut" (8..15 outside, folded onto
-// 7); TMA zero-fills the outside samples — then f32 Dw (S5), bf16 Dw (S7)
-constexpr uint32_t kOffB1 = kOffB, kOffB1L = kOffB + 1536, kOffB5 = kOffB + 3072,
-                   kOffB7 = kOffB + 4096;
-constexpr uint32_t kConstBytes = 4608;
-constexpr uint32_t kOffBar = kOffB + kConstBytes;
+constexpr uint32_t kOffC = kOffOut + ((kOutBytes + 1023) / 1024) * 1024;
+// constants (built on the host, one bulk copy per CTA):
+//   S1 strips: [p][hi/lo] 240 rows x 16 K, K-major core matrices (7680 B each)
+//   S7 strip : 248 rows x 16 K
+//   B3       : Dwᵀ as the S3 B operand (K = sample, N = freq), hi + lo
+//   B5       : Dw f32 (K = freq, N = sample) for S5
+constexpr uint32_t kStripBytes = 7680;
+constexpr uint32_t kCS7 = 4 * kStripBytes;
+constexpr uint32_t kCB3 = kCS7 + 7936;
+constexpr uint32_t kCB5 = kCB3 + 1024;
+constexpr uint32_t kConstBytes = kCB5 + 1024;
+constexpr uint32_t kOffBar = kOffC + kConstBytes;
 constexpr uint32_t kSmem = kOffBar + 256 + 1024;
+
+// TMEM columns
+constexpr uint32_t kTD1 = 0;    // D1 f32 / packed pairs (hi 0..63, lo 64..127) / D3
+constexpr uint32_t kTD2 = 128;  // 240 columns
+constexpr uint32_t kTD4 = 368;  // 128 columns
 
 struct Params {
   int planes, H, W, nry, nrx, nregions;
   float threshold;
   int soft;                 // 0 hard, 1 soft coring
-  const uint8_t* consts;    // kConstBytes: the three B tiles in smem layout
+  const uint8_t* consts;    // kConstBytes
   float* dbg;               // diagnostics: [4 stages][2 phases][128 lanes][256] for CTA 0, band 0
+  unsigned long long* trace;  // diagnostics (ts_debug_trace): clock64 per (CTA, band, event), 24 events
+  int trace_ctas, trace_tiles;
 };
+
+// events: 12p + {0 D1 seen, 1 C1 done, 2 D2 seen, 3 E2 done, 4 D3 seen, 5 E3 done};
+// 7 MMA: band ready, 8 MMA: S1 issued (p=0); 22 E4 start, 23 E4 stored
+__device__ __forceinline__ void stamp(const Params& P, int it, int ev) {
+  if (P.trace != nullptr && static_cast<int>(blockIdx.x) < P.trace_ctas && it < P.trace_tiles)
+    P.trace[(static_cast<size_t>(blockIdx.x) * P.trace_tiles + it) * 24 + ev] = clock64();
+}
 
 // Diagnostics: copy `ncols` TMEM columns of this thread's lane to dbg.
 __device__ __forceinline__ void dbg_dump(const Params& P, int it, int stage, int p, uint32_t taddr,
@@ -89,20 +111,20 @@ __device__ __forceinline__ void dbg_dump(const Params& P, int it, int stage, int
   }
 }
 
-__device__ __forceinline__ void mma_tf32_ss_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                                  uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
 __device__ __forceinline__ void mma_tf32_ts_elect(uint32_t d, uint32_t a_tmem, uint64_t b,
                                                   uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_f16_ts_elect(uint32_t d, uint32_t a_tmem, uint64_t b,
+                                                 uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
@@ -117,39 +139,50 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
-// bf16 MN-major 128B-swizzled operand: M = 128 (2 atoms of 64 at 16 KB),
-// K = 128 (16 groups of 8 rows at 1 KB).  Address of the 16-byte chunk
-// holding m = 8*m8 .. 8*m8+7 at K row k.
-__device__ __forceinline__ uint32_t opbf_chunk(uint32_t base, int m8, int k) {
-  return base + (m8 / 8) * 16384u + (k / 8) * 1024u + (k % 8) * 128u +
-         ((((m8 % 8) ^ (k % 8))) * 16u);
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// Write 16 consecutive-M f32 values of K row k as bf16 hi/lo pairs.
-__device__ __forceinline__ void put_hilo16(uint32_t op_s, int m8_first, int k,
-                                           const uint32_t (&r)[16]) {
-#pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    uint32_t hi[4], lo[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float a = __uint_as_float(r[8 * g + 2 * e]), b = __uint_as_float(r[8 * g + 2 * e + 1]);
-      const __nv_bfloat16 ah = __float2bfloat16_rn(a), bh = __float2bfloat16_rn(b);
-      hi[e] = pack_bf16x2(a, b);
-      lo[e] = pack_bf16x2(a - __bfloat162float(ah), b - __bfloat162float(bh));
+// Byte offset of element (row, col) in a 128-row x 128-col bf16 operand made
+// of two 64-column 128B-swizzled halves (the TMA band layout, and B7).
+__device__ __forceinline__ uint32_t sw_off(int row, int col) {
+  return (col >> 6) * 16384u + row * 128u + ((((col & 63) >> 3) ^ (row & 7)) << 4) + (col & 7) * 2u;
+}
+
+__device__ __forceinline__ uint32_t hi_lo(float a, float b, uint32_t* lo) {
+  const __nv_bfloat16 ah = __float2bfloat16_rn(a), bh = __float2bfloat16_rn(b);
+  *lo = pack_bf16x2(a - __bfloat162float(ah), b - __bfloat162float(bh));
+  return pack_bf16x2(a, b);
+}
+
+// Clamp-to-edge for border bands: replicate the edge row / column of the
+// image into the (TMA zero-filled) 8 samples beyond it.  Whole warp.
+__device__ __forceinline__ void fix_edges(uint8_t* bx, int Y, int X, int H, int W, int lane) {
+  int r0[2], rs[2], nr = 0;
+  if (Y == 0) { r0[nr] = 0; rs[nr] = 8; ++nr; }
+  if (H - Y + 8 < kBand) { r0[nr] = H - Y + 8; rs[nr] = H - Y + 7; ++nr; }
+  for (int e = 0; e < nr; ++e) {
+    const int rows = min(8, kBand - r0[e]);
+    for (int idx = lane; idx < rows * 16; idx += 32) {
+      const int br = r0[e] + idx / 16, j = idx % 16, h = j >> 3, cc = j & 7;
+      const uint4 v = *reinterpret_cast<const uint4*>(bx + h * 16384 + rs[e] * 128 +
+                                                      ((cc ^ (rs[e] & 7)) << 4));
+      *reinterpret_cast<uint4*>(bx + h * 16384 + br * 128 + ((cc ^ (br & 7)) << 4)) = v;
     }
-    const uint32_t addr = opbf_chunk(op_s, m8_first + g, k);
-    st_shared_v4(addr, hi[0], hi[1], hi[2], hi[3]);
-    st_shared_v4(addr + kOpLo, lo[0], lo[1], lo[2], lo[3]);
   }
-}
-
-// Edge variant of a 16-sample tile starting at image coordinate x0 (multiple
-// of 8) on an axis of length n (multiple of 8).
-__device__ __forceinline__ uint32_t edge_variant(int x0, int n) {
-  if (x0 < 0 && x0 + 16 > 0) return 1u;
-  if (x0 < n && x0 + 16 > n) return 2u;
-  return 0u;
+  __syncwarp();
+  int c0[2], cs[2], nc = 0;
+  if (X == 0) { c0[nc] = 0; cs[nc] = 8; ++nc; }
+  if (W - X + 8 < kBand) { c0[nc] = W - X + 8; cs[nc] = W - X + 7; ++nc; }
+  for (int e = 0; e < nc; ++e) {
+    for (int br = lane; br < kBand; br += 32) {
+      const uint32_t v = *reinterpret_cast<const uint16_t*>(bx + sw_off(br, cs[e]));
+      const uint32_t w = v | (v << 16);
+      *reinterpret_cast<uint4*>(bx + sw_off(br, c0[e])) = make_uint4(w, w, w, w);
+    }
+  }
+  fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05 operand reads
+  __syncwarp();
 }
 
 struct Region {
@@ -165,10 +198,10 @@ __device__ __forceinline__ Region region_of(const Params& P, int t) {
   return r;
 }
 
-template <typename OutT>
+template <typename OutT, bool SOFT>
 __global__ void __launch_bounds__(kThreads, 1)
     dct16_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                 const Params P) {
+                 const __grid_constant__ Params P) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_s = smem_u32(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
@@ -176,31 +209,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + kOffBar);
   uint64_t* xfull = bars;        // [2]
   uint64_t* xempty = bars + 2;   // [2]
-  uint64_t* b_s1 = bars + 4;
-  uint64_t* b_s3 = bars + 5;
-  uint64_t* b_s5 = bars + 6;
-  uint64_t* b_s7 = bars + 7;
-  uint64_t* e1 = bars + 8;
+  uint64_t* xready = bars + 4;   // [2]
+  uint64_t* s1done = bars + 6;
+  uint64_t* c1 = bars + 7;
+  uint64_t* s3done = bars + 8;
   uint64_t* e2 = bars + 9;
-  uint64_t* e3 = bars + 10;
-  uint64_t* e4 = bars + 11;
-  uint64_t* cbar = bars + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* s5done = bars + 10;
+  uint64_t* e3 = bars + 11;
+  uint64_t* s7done = bars + 12;
+  uint64_t* e4 = bars + 13;
+  uint64_t* cbar = bars + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&xfull[s], 1);
       mbar_init(&xempty[s], 1);
+      mbar_init(&xready[s], 1);
     }
-    mbar_init(b_s1, 1);
-    mbar_init(b_s3, 1);
-    mbar_init(b_s5, 1);
-    mbar_init(b_s7, 1);
-    mbar_init(e1, 128);
-    mbar_init(e2, 128);
-    mbar_init(e3, 128);
-    mbar_init(e4, 128);
+    mbar_init(s1done, 1);
+    mbar_init(s3done, 1);
+    mbar_init(s5done, 1);
+    mbar_init(s7done, 1);
+    mbar_init(c1, kEpiThreads);
+    mbar_init(e2, kEpiThreads);
+    mbar_init(e3, kEpiThreads);
+    mbar_init(e4, kEpiThreads);
     mbar_init(cbar, 1);
     fence_barrier_init();
     prefetch_tmap(&tm_in);
@@ -211,204 +246,259 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: [0,256) D1 / D2, [256,384) D3, [384,512) D4
-  const uint32_t tD1 = tmem, tD2 = tmem, tD3 = tmem + 256u, tD4 = tmem + 384u;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ loader + edge fix-up
     if (lane == 0) {
       mbar_arrive_expect_tx(cbar, kConstBytes);
-      bulk_g2s(base + kOffB, P.consts, kConstBytes, cbar);
-      int it = 0;
-      for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
-        const int s = it & 1;
-        mbar_wait(&xempty[s], ((it >> 1) & 1) ^ 1);
-        const Region R = region_of(P, t);
-        const int Y = R.ry * kOut, X = R.rx * kOut;
-        mbar_arrive_expect_tx(&xfull[s], kBandBytes);
-        uint8_t* dst = base + kOffX + s * kBandBytes;
-        tma_load_3d(dst, &tm_in, &xfull[s], X - 8, Y - 8, R.p);
-        tma_load_3d(dst + kBand * 128, &tm_in, &xfull[s], X - 8 + 64, Y - 8, R.p);
-      }
+      bulk_g2s(base + kOffC, P.consts, kConstBytes, cbar);
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    const uint32_t id_bf = make_idesc(kFmtBF16, 128, 16, /*A MN*/ 1, 0);
-    const uint32_t id_tf_k = make_idesc(kFmtTF32, 128, 16, 0, 0);
-    // B descriptors (K-major, no swizzle): bf16 16x16 (LBO 128, SBO 256);
-    // f32 16x16 (core matrices 8 n x 4 k: LBO 128, SBO 512)
-    const uint64_t bd1 = make_sdesc(base_s + kOffB1, 128u, 256u, kSwizzleNone);
-    const uint64_t bd1l = make_sdesc(base_s + kOffB1L, 128u, 256u, kSwizzleNone);
-    const uint64_t bd5 = make_sdesc(base_s + kOffB5, 128u, 512u, kSwizzleNone);
-    const uint64_t bd7 = make_sdesc(base_s + kOffB7, 128u, 256u, kSwizzleNone);
-    const uint32_t op_s = base_s + kOffOp;
-    mbar_wait(cbar, 0);
     int it = 0;
-    uint32_t ph_e = 0;  // phase of e1/e2/e3 (each completes twice per region)
     for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
       const int s = it & 1;
       const Region R = region_of(P, t);
       const int Y = R.ry * kOut, X = R.rx * kOut;
+      uint8_t* dst = base + kOffX + s * kBandBytes;
+      if (lane == 0) {
+        mbar_wait(&xempty[s], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&xfull[s], kBandBytes);
+        tma_load_3d(dst, &tm_in, &xfull[s], X - 8, Y - 8, R.p);
+        tma_load_3d(dst + kBand * 128, &tm_in, &xfull[s], X - 8 + 64, Y - 8, R.p);
+      }
+      __syncwarp();
+      const bool edge = Y == 0 || X == 0 || P.H - Y + 8 < kBand || P.W - X + 8 < kBand;
+      if (edge) {
+        mbar_wait(&xfull[s], (it >> 1) & 1);
+        fix_edges(dst, Y, X, P.H, P.W, lane);
+      }
+      if (lane == 0) mbar_arrive(&xready[s]);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t id128 = make_idesc(kFmtBF16, 128, 128, /*A K-major*/ 0, /*B MN*/ 1);
+    const uint32_t id16 = make_idesc(kFmtBF16, 128, 16, 0, 0);
+    const uint32_t idtf = make_idesc(kFmtTF32, 128, 16, 0, 0);
+    const uint64_t a_tmpl = make_sdesc(0u, 128u, 256u, kSwizzleNone);
+    const uint32_t c4 = (base_s + kOffC) >> 4;
+    const uint64_t b3 = make_sdesc(base_s + kOffC + kCB3, 128u, 256u, kSwizzleNone);
+    const uint64_t b5 = make_sdesc(base_s + kOffC + kCB5, 128u, 512u, kSwizzleNone);
+    const uint64_t b7 = make_sdesc(base_s + kOffB7, 16384u, 1024u, kSwizzle128B);
+    mbar_wait(cbar, 0);
+    int it = 0;
+    uint32_t ph = 0;  // phase of the per-row-phase barriers (two completions per band)
+    for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
+      const int s = it & 1;
       mbar_wait(&xfull[s], (it >> 1) & 1);
-      const uint32_t band_s = base_s + kOffX + s * kBandBytes;
+      mbar_wait(&xready[s], (it >> 1) & 1);
+      if (lane == 0) stamp(P, it, 7);
+      const uint64_t bx = make_sdesc(base_s + kOffX + s * kBandBytes, 16384u, 1024u, kSwizzle128B);
+#pragma unroll
       for (int p = 0; p < 2; ++p) {
-        const int ni = p == 0 ? 8 : 7;
-        // ---- S1: column forward (A = band MN-major: M = cols, K = rows)
-        if (p == 1) mbar_wait(b_s7, 0 ^ (static_cast<uint32_t>(it * 2) & 1));  // S7_0 done: S_R free
+        // ---- S1: D1 = T_p · X  (8 K-steps of 16 band rows, A strip hi + lo)
         tc_fence_after();
-        for (int i = 0; i < ni; ++i) {
-          const uint64_t ad =
-              make_sdesc(band_s + (16u * i + 8u * p) * 128u, kBand * 128u, 1024u, kSwizzle128B);
-          const uint32_t v = edge_variant(Y - 8 + 16 * i + 8 * p, P.H);
-          mma_f16_ss_elect(tD1 + 16u * i, ad, bd1 + 32u * v, id_bf, 0u);
-          mma_f16_ss_elect(tD1 + 16u * i, ad, bd1l + 32u * v, id_bf, 1u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t so = (14u - 2u * k) * 16u;  // strip offset, 16-byte units
+          mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + (2 * p) * (kStripBytes / 16) + so),
+                           bx + 128u * k, id128, k > 0 ? 1u : 0u);
+          mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + (2 * p + 1) * (kStripBytes / 16) + so),
+                           bx + 128u * k, id128, 1u);
         }
-        mma_commit_elect(b_s1);
+        mma_commit_elect(s1done);
+        if (p == 0 && lane == 0) stamp(P, it, 8);
         if (p == 1) mma_commit_elect(&xempty[s]);
-        // ---- S3: row forward (A = S_Y hi/lo MN-major: M = freq-row, K = col)
-        mbar_wait(e1, ph_e);
+        // ---- S3: row forward, A = packed D1 from TMEM
+        mbar_wait(c1, ph);
         tc_fence_after();
+#pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const int nj = q == 0 ? 8 : 7;
-          for (int j = 0; j < nj; ++j) {
-            const uint32_t kc = 16u * j + 8u * q;  // first column of the tile
-            const uint64_t ad = make_sdesc(op_s + (kc / 8u) * 1024u, 16384u, 1024u, kSwizzle128B);
-            const uint64_t adl =
-                make_sdesc(op_s + kOpLo + (kc / 8u) * 1024u, 16384u, 1024u, kSwizzle128B);
-            const uint32_t v = edge_variant(X - 8 + static_cast<int>(kc), P.W);
-            mma_f16_ss_elect(tD2 + 16u * (8 * q + j), ad, bd1 + 32u * v, id_bf, 0u);
-            mma_f16_ss_elect(tD2 + 16u * (8 * q + j), adl, bd1 + 32u * v, id_bf, 1u);
-            mma_f16_ss_elect(tD2 + 16u * (8 * q + j), ad, bd1l + 32u * v, id_bf, 1u);
+#pragma unroll
+          for (int j = 0; j < (q == 0 ? 8 : 7); ++j) {
+            const uint32_t pc = 8u * j + 4u * q;  // packed column of the tile's first sample
+            const uint32_t d = tmem + kTD2 + 16u * (8 * q + j);
+            mma_f16_ts_elect(d, tmem + kTD1 + pc, b3, id16, 0u);
+            mma_f16_ts_elect(d, tmem + kTD1 + 64u + pc, b3, id16, 1u);
+            mma_f16_ts_elect(d, tmem + kTD1 + pc, b3 + 32u, id16, 1u);
           }
         }
-        mma_commit_elect(b_s3);
-        // ---- S5: row inverse (A = cored D2 from TMEM, K = freq l)
-        mbar_wait(e2, ph_e);
+        mma_commit_elect(s3done);
+        // ---- S5: row inverse (TS tf32, A = cored D2) into D3 (over D1)
+        mbar_wait(e2, ph);
         tc_fence_after();
+#pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const int nj = q == 0 ? 8 : 7;
-          for (int j = 0; j < nj; ++j) {
-            const uint32_t c0 = 16u * j + 8u * q;
+#pragma unroll
+          for (int j = 0; j < (q == 0 ? 8 : 7); ++j) {
+#pragma unroll
             for (int h = 0; h < 2; ++h)
-              mma_tf32_ts_elect(tD3 + c0, tD2 + 16u * (8 * q + j) + 8u * h, bd5 + 16u * h,
-                                id_tf_k, (q > 0 || h > 0) ? 1u : 0u);
+              mma_tf32_ts_elect(tmem + kTD1 + 16u * j + 8u * q, tmem + kTD2 + 16u * (8 * q + j) + 8u * h,
+                                b5 + 16u * h, idtf, (q > 0 || h > 0) ? 1u : 0u);
           }
         }
-        mma_commit_elect(b_s5);
-        // ---- S7: column inverse (A = S_R hi/lo MN-major: M = col, K = freq-row)
-        mbar_wait(e3, ph_e);
-        if (p == 0 && it > 0) mbar_wait(e4, (it - 1) & 1);  // previous E4 read D4
+        mma_commit_elect(s5done);
+        // ---- S7: column inverse, D4 += T_pᵀ · B7 (hi + lo)
+        mbar_wait(e3, ph);
+        if (p == 0 && it > 0) mbar_wait(e4, (it - 1) & 1);  // previous band's E4 read D4
         tc_fence_after();
-        for (int i = 0; i < ni; ++i) {
-          const uint64_t ad = make_sdesc(op_s + (2u * i) * 1024u, 16384u, 1024u, kSwizzle128B);
-          const uint64_t adl =
-              make_sdesc(op_s + kOpLo + (2u * i) * 1024u, 16384u, 1024u, kSwizzle128B);
-          mma_f16_ss_elect(tD4 + 16u * i + 8u * p, ad, bd7, id_bf, p > 0 ? 1u : 0u);
-          mma_f16_ss_elect(tD4 + 16u * i + 8u * p, adl, bd7, id_bf, 1u);
+#pragma unroll
+        for (int k = 0; k < (p == 0 ? 8 : 7); ++k) {
+          const uint64_t ad = a_tmpl | (c4 + kCS7 / 16 + (15u - 2u * k - p) * 16u);
+          mma_f16_ss_elect(tmem + kTD4, ad, b7 + 128u * k, id128, (p > 0 || k > 0) ? 1u : 0u);
+          mma_f16_ss_elect(tmem + kTD4, ad, b7 + 128u * k + kB7Lo / 16, id128, 1u);
         }
-        mma_commit_elect(b_s7);
-        ph_e ^= 1;
+        mma_commit_elect(s7done);
+        ph ^= 1;
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2-5)
+    // ------------------------------------------------------------ epilogue (warps 2-17)
+    // 16 warps: warp w serves TMEM lane quarter w % 4 (hardware rule) and
+    // column split sp = (w - 2) / 4, so each step's ALU work is spread over
+    // four warps per scheduler.
     const int quarter = warp & 3;
+    const int sp = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;  // TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t op_s = base_s + kOffOp;
+    const uint32_t tl = tmem + lane_off;
     const int et = threadIdx.x - 64;
     int it = 0;
-    uint32_t ph = 0;  // phase of b_s1/b_s3/b_s5/b_s7 (each completes twice per region)
+    uint32_t ph = 0;
     for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
       const Region R = region_of(P, t);
       const int Y = R.ry * kOut, X = R.rx * kOut;
       for (int p = 0; p < 2; ++p) {
-        // ---- E1: D1 (lane = col c) -> S_Y[m][c] f32 MN-major (M = m, K = c)
-        mbar_wait(b_s1, ph);
+        // ---- C1: D1 (f32, lane f, 128 columns) -> bf16 pairs: hi at 0..63, lo at 64..127
+        mbar_wait(s1done, ph);
         tc_fence_after();
-        dbg_dump(P, it, 0, p, tD1 + lane_off, row, 128);
-        for (int ch = 0; ch < 8; ++ch) {
-          uint32_t r[16];
-          tmem_ld16(tD1 + lane_off + 16u * ch, r);
+        if (et == 0) stamp(P, it, 12 * p + 0);
+        if (sp == 0) dbg_dump(P, it, 0, p, tl + kTD1, row, 128);
+        {
+          uint32_t v[2][16];
+          tmem_ld16(tl + kTD1 + 32u * sp, v[0]);
+          tmem_ld16(tl + kTD1 + 32u * sp + 16u, v[1]);
           tmem_wait_ld();
-          put_hilo16(op_s, 2 * ch, row, r);  // M = freq-row 16ch.., K = this column
+          named_bar_sync(1, kEpiThreads);  // every split has read its f32 columns
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            hi[e] = hi_lo(__uint_as_float(v[e >> 3][(2 * e) & 15]),
+                          __uint_as_float(v[e >> 3][((2 * e) & 15) + 1]), &lo[e]);
+          tmem_st16(tl + kTD1 + 16u * sp, hi);
+          tmem_st16(tl + kTD1 + 64u + 16u * sp, lo);
         }
+        tmem_wait_st();
         tc_fence_before();
-        fence_proxy_async_smem();
-        mbar_arrive(e1);
-        // ---- E2: coring of D2 (lane = freq-row m, cols = 16*(8q+j) + l) in place
-        mbar_wait(b_s3, ph);
+        mbar_arrive(c1);
+        if (et == 0) stamp(P, it, 12 * p + 1);
+        // ---- E2: coring of D2 (lane f, columns 16*(8q+j) + l) in place
+        mbar_wait(s3done, ph);
         tc_fence_after();
-        dbg_dump(P, it, 1, p, tD2 + lane_off, row, 240);
-        for (int ch = 0; ch < 15; ++ch) {
-          uint32_t r[16];
-          tmem_ld16(tD2 + lane_off + 16u * ch, r);
+        if (et == 0) stamp(P, it, 12 * p + 2);
+        if (sp == 0) dbg_dump(P, it, 1, p, tl + kTD2, row, 240);
+        {
+          const bool dc_row = (row & 15) == 0;
+          const float thr = P.threshold;
+          uint32_t v[4][16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (sp + 4 * c < 15) tmem_ld16(tl + kTD2 + 16u * (sp + 4 * c), v[c]);
           tmem_wait_ld();
 #pragma unroll
-          for (int l = 0; l < 16; ++l) {
-            float v = __uint_as_float(r[l]);
-            const bool dc = (row % 16 == 0) && (l == 0);
-            if (!dc) {
-              if (P.soft)
-                v = copysignf(fmaxf(fabsf(v) - P.threshold, 0.0f), v);
-              else if (fabsf(v) < P.threshold)
-                v = 0.0f;
+          for (int c = 0; c < 4; ++c) {
+            if (sp + 4 * c < 15) {
+              const uint32_t dc = v[c][0];
+#pragma unroll
+              for (int l = 0; l < 16; ++l) {
+                const float x = __uint_as_float(v[c][l]);
+                float y;
+                if constexpr (SOFT)
+                  y = copysignf(fmaxf(fabsf(x) - thr, 0.0f), x);
+                else
+                  y = fabsf(x) < thr ? 0.0f : x;
+                v[c][l] = __float_as_uint(y);
+              }
+              if (dc_row) v[c][0] = dc;  // DC coefficient kept
+              tmem_st16(tl + kTD2 + 16u * (sp + 4 * c), v[c]);
             }
-            r[l] = __float_as_uint(v);
           }
-          tmem_st16(tD2 + lane_off + 16u * ch, r);
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tmem_wait_st();
         tc_fence_before();
         mbar_arrive(e2);
-        // ---- E3: D3 (lane = m, cols = band col c) -> S_R[c][m] f32 MN-major (M = c, K = m)
-        mbar_wait(b_s5, ph);
+        if (et == 0) stamp(P, it, 12 * p + 3);
+        // ---- E3: D3 (lane f, 128 columns) -> B7[f][c] hi/lo (MN-major, 128B swizzle)
+        mbar_wait(s5done, ph);
         tc_fence_after();
-        dbg_dump(P, it, 2, p, tD3 + lane_off, row, 128);
-        for (int ch = 0; ch < 8; ++ch) {
-          uint32_t r[16];
-          tmem_ld16(tD3 + lane_off + 16u * ch, r);
+        if (et == 0) stamp(P, it, 12 * p + 4);
+        if (sp == 0) dbg_dump(P, it, 2, p, tl + kTD1, row, 128);
+        {
+          uint8_t* b7 = base + kOffB7;
+          uint32_t v[2][16];
+          tmem_ld16(tl + kTD1 + 32u * sp, v[0]);
+          tmem_ld16(tl + kTD1 + 32u * sp + 16u, v[1]);
           tmem_wait_ld();
-          put_hilo16(op_s, 2 * ch, row, r);  // M = band col 16ch.., K = this freq-row
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              hi[e] = hi_lo(__uint_as_float(v[g >> 1][8 * (g & 1) + 2 * e]),
+                            __uint_as_float(v[g >> 1][8 * (g & 1) + 2 * e + 1]), &lo[e]);
+            const uint32_t off = sw_off(row, 32 * sp + 8 * g);
+            *reinterpret_cast<uint4*>(b7 + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(b7 + kB7Lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
         }
         tc_fence_before();
         fence_proxy_async_smem();
         mbar_arrive(e3);
-        // next phase's E1 overwrites S_Y = S_R: wait for S7 of this phase
-        mbar_wait(b_s7, ph);
+        if (et == 0) stamp(P, it, 12 * p + 5);
         ph ^= 1;
       }
-      // ---- E4: D4 (lane = band col c, cols = band row) -> output block
+      // ---- E4: D4 (lane = band row r, columns = band column c) -> output block
+      mbar_wait(s7done, ph ^ 1);
       tc_fence_after();
-      dbg_dump(P, it, 3, 0, tD4 + lane_off, row, 128);
+      if (et == 0) stamp(P, it, 22);
+      if (sp == 0) dbg_dump(P, it, 3, 0, tl + kTD4, row, 128);
       if (et == 0) bulk_wait_read0();
-      named_bar_sync(1, 128);
-      OutT* stg = reinterpret_cast<OutT*>(base + kOffOut);
-      for (int ch = 0; ch < 8; ++ch) {
-        uint32_t r[16];
-        tmem_ld16(tD4 + lane_off + 16u * ch, r);
+      named_bar_sync(1, kEpiThreads);
+      {
+        uint32_t v[2][16];
+        tmem_ld16(tl + kTD4 + 32u * sp, v[0]);
+        tmem_ld16(tl + kTD4 + 32u * sp + 16u, v[1]);
         tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(e4);
         if (row >= 8 && row < 8 + kOut) {
+          uint8_t* orow = base + kOffOut + (row - 8) * kOut * sizeof(OutT);
+          // band columns 8..119 -> output columns 0..111, 8 at a time
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int br = ch * 16 + e;
-            if (br >= 8 && br < 8 + kOut) {
-              const float v = __uint_as_float(r[e]);
-              if constexpr (sizeof(OutT) == 2)
-                stg[(br - 8) * kOut + (row - 8)] = __float2bfloat16_rn(v);
-              else
-                stg[(br - 8) * kOut + (row - 8)] = v;
+          for (int g = 0; g < 4; ++g) {
+            const int c = 32 * sp + 8 * g;
+            if (c >= 8 && c < 8 + kOut) {
+              const uint32_t* src = &v[g >> 1][8 * (g & 1)];
+              if constexpr (sizeof(OutT) == 2) {
+                *reinterpret_cast<uint4*>(orow + (c - 8) * 2) =
+                    make_uint4(pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1])),
+                               pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3])),
+                               pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5])),
+                               pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7])));
+              } else {
+                *reinterpret_cast<uint4*>(orow + (c - 8) * 4) =
+                    make_uint4(src[0], src[1], src[2], src[3]);
+                *reinterpret_cast<uint4*>(orow + (c - 8) * 4 + 16) =
+                    make_uint4(src[4], src[5], src[6], src[7]);
+              }
             }
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(e4);
       fence_proxy_async_smem();
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kEpiThreads);
       if (et == 0) {
-        tma_store_3d(&tm_out, stg, X, Y, R.p);
+        tma_store_3d(&tm_out, base + kOffOut, X, Y, R.p);
         bulk_commit();
+        stamp(P, it, 23);
       }
     }
     if (et == 0) bulk_wait0();
@@ -426,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 static float* g_dct_dbg = nullptr;
 void dct_set_debug(float* p) { g_dct_dbg = p; }
 
-// Host: the constant B tiles in their smem byte layout.
+// Host: the constant operands in their smem byte layouts.
 static void build_consts(uint8_t* out) {
   double D[16][16], w[16];
   for (int m = 0; m < 16; ++m) w[m] = std::sin(3.14159265358979323846 * (m + 0.5) / 16.0);
@@ -446,40 +536,50 @@ static void build_consts(uint8_t* out) {
     std::memcpy(&f, &b, 4);
     return static_cast<double>(f);
   };
-  // lo = 0: bf16(v); lo = 1: bf16(v - bf16(v))
-  auto put16 = [&](uint8_t* dst, int kk, int n, double v, int lo) {
+  // K-major no-swizzle core matrices, 16 K: element (row n, k) of a bf16 operand
+  auto put16 = [&](uint8_t* dst, int n, int kk, double v, int lo) {
     uint16_t h = bf16_bits(v);
     if (lo) h = bf16_bits(v - bf16_val(h));
     std::memcpy(dst + (n / 8) * 256 + (kk / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2, &h, 2);
   };
   // f32 K-major core matrices (8 n x 4 k): (n/8)*512 + (k/4)*128 + (n%8)*16 + (k%4)*4
-  auto put32 = [&](uint8_t* dst, int kk, int n, double v) {
+  auto put32 = [&](uint8_t* dst, int n, int kk, double v) {
     const float f = static_cast<float>(v);
     std::memcpy(dst + (n / 8) * 512 + (kk / 4) * 128 + (n % 8) * 16 + (kk % 4) * 4, &f, 4);
   };
-  for (int v = 0; v < 3; ++v) {
-    // B1[K = sample][N = freq] = Dw[freq][sample], edge-folded (variant v)
-    double F[16][16];
-    for (int n = 0; n < 16; ++n)
-      for (int kk = 0; kk < 16; ++kk) F[n][kk] = D[n][kk];
-    for (int n = 0; n < 16; ++n) {
-      if (v == 1) {
-        for (int kk = 0; kk < 8; ++kk) { F[n][8] += F[n][kk]; F[n][kk] = 0; }
-      } else if (v == 2) {
-        for (int kk = 8; kk < 16; ++kk) { F[n][7] += F[n][kk]; F[n][kk] = 0; }
-      }
-    }
-    for (int kk = 0; kk < 16; ++kk)
-      for (int n = 0; n < 16; ++n) {
-        put16(out + 512 * v, kk, n, F[n][kk], 0);         // hi
-        put16(out + 1536 + 512 * v, kk, n, F[n][kk], 1);  // lo
+  // S1 strips: row g, K = band row within the K-step.  Step k reads rows
+  // g = f + 112 - 16k, so tile i = k sits at g in [112, 128).
+  for (int lo = 0; lo < 2; ++lo) {
+    uint8_t* s0 = out + (0 * 2 + lo) * dct::kStripBytes;
+    uint8_t* s1 = out + (1 * 2 + lo) * dct::kStripBytes;
+    for (int k = 0; k < 16; ++k)
+      for (int kk = 0; kk < 16; ++kk) {
+        put16(s0, 112 + k, kk, D[k][kk], lo);                       // p = 0: tile rows 16i..
+        if (kk < 8) put16(s1, 96 + k, kk, D[k][kk + 8], lo);      // p = 1: tile i-1, 2nd half
+        if (kk >= 8) put16(s1, 112 + k, kk, D[k][kk - 8], lo);    // p = 1: tile i, 1st half
       }
   }
-  for (int kk = 0; kk < 16; ++kk)
-    for (int n = 0; n < 16; ++n) {
-      put32(out + 3072, kk, n, D[kk][n]);    // B5[K=l][N=c] = Dw[l][c] (S5, f32)
-      put16(out + 4096, kk, n, D[kk][n], 0); // B7[K=k][N=r] = Dw[k][r] (S7)
+  // S7 strip: A7[r][kk] = Dw[kk][r - 16k - 8p] at g = r + 120 - 16k - 8p
+  for (int m = 0; m < 16; ++m)
+    for (int kk = 0; kk < 16; ++kk) put16(out + dct::kCS7, 120 + m, kk, D[kk][m], 0);
+  // B3[K = sample c][N = freq l] = Dw[l][c]: hi, lo
+  for (int l = 0; l < 16; ++l)
+    for (int c = 0; c < 16; ++c) {
+      put16(out + dct::kCB3, l, c, D[l][c], 0);
+      put16(out + dct::kCB3 + 512, l, c, D[l][c], 1);
     }
+  // B5[K = freq l][N = sample c] = Dw[l][c] (f32)
+  for (int c = 0; c < 16; ++c)
+    for (int l = 0; l < 16; ++l) put32(out + dct::kCB5, c, l, D[l][c]);
+}
+
+template <typename OutT, bool SOFT>
+static cudaError_t launch_dct(int grid, const CUtensorMap& tin, const CUtensorMap& tout,
+                              const dct::Params& P, cudaStream_t stream) {
+  auto k = dct::dct16_kernel<OutT, SOFT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dct::kSmem);
+  if (e == cudaSuccess) k<<<grid, dct::kThreads, dct::kSmem, stream>>>(tin, tout, P);
+  return e;
 }
 
 ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, void* out,
@@ -518,6 +618,7 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
   P.soft = soft;
   P.consts = d_consts[dev];
   P.dbg = g_dct_dbg;
+  get_trace(&P.trace, &P.trace_ctas, &P.trace_tiles);
   CUtensorMap tin, tout;
   ts_status st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs,
                                 in_ps, 64, dct::kBand, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -531,17 +632,12 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
   const int sms = sm_count_current();
   const int grid = P.nregions < sms ? P.nregions : sms;
   cudaError_t e;
-  if (out_dtype == TS_BF16) {
-    e = cudaFuncSetAttribute(dct::dct16_kernel<__nv_bfloat16>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, dct::kSmem);
-    if (e == cudaSuccess)
-      dct::dct16_kernel<__nv_bfloat16><<<grid, dct::kThreads, dct::kSmem, stream>>>(tin, tout, P);
-  } else {
-    e = cudaFuncSetAttribute(dct::dct16_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             dct::kSmem);
-    if (e == cudaSuccess)
-      dct::dct16_kernel<float><<<grid, dct::kThreads, dct::kSmem, stream>>>(tin, tout, P);
-  }
+  if (out_dtype == TS_BF16)
+    e = soft ? launch_dct<__nv_bfloat16, true>(grid, tin, tout, P, stream)
+             : launch_dct<__nv_bfloat16, false>(grid, tin, tout, P, stream);
+  else
+    e = soft ? launch_dct<float, true>(grid, tin, tout, P, stream)
+             : launch_dct<float, false>(grid, tin, tout, P, stream);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "dct16 launch");
 }
