@@ -120,6 +120,20 @@ TS_API ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int 
                            int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
                            void* stream);
 
+/* One banded axis along rows (dim = 0: out is a->n_out x width) or columns
+ * (dim = 1: out is height x a->n_out) of `planes` bf16 planes; out bf16 or
+ * f32.  Any window up to 1024 inputs per 16 outputs (the K window streams
+ * through a TMA ring).  ts_separable_run reports TS_ERR_UNSUPPORTED for
+ * axes whose windows do not fit its fused tile (large downscale factors,
+ * very wide filters); those run as two axis passes with a bf16
+ * intermediate, the rounding point of the fused kernel's intermediate.
+ * Replaces, for such geometries, the per-tile loop of interp.run_program
+ * (interp.py:570-619) like ts_separable_run does. */
+TS_API ts_status ts_axis_pass(const ts_axis* a, int dim, int planes, int height, int width,
+                              const void* in, int64_t in_row_stride, int64_t in_plane_stride,
+                              void* out, int64_t out_row_stride, int64_t out_plane_stride,
+                              int out_dtype, void* stream);
+
 /* Launch geometry ts_separable_run would use for these axes:
  * out8 = {stages, V buffers, weights resident (0/1), smem bytes, staged rows
  * per tile, column blocks per tile, tiles, grid CTAs}. */

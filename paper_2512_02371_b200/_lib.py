@@ -70,6 +70,7 @@ _SIGNATURES = {
     "ts_separable_run": (_I, [_P, _P, _I, _P, _I64, _I64, _I, _P, _I64, _I64, _I, _P]),
     "ts_separable_plan": (_I, [_P, _P, _I, _I, ctypes.POINTER(ctypes.c_int)]),
     "ts_separable_variant": (_I, [_P, _P, _I, _I]),
+    "ts_axis_pass": (_I, [_P, _I, _I, _I, _I, _P, _I64, _I64, _P, _I64, _I64, _I, _P]),
     "ts_strip_info": (_I, [ctypes.POINTER(ctypes.c_int)]),
     "ts_probe_tma": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P]),
     "ts_probe_issue2": (_I, [_I, _I, _I, _I, _I, _P, _P]),

@@ -1,0 +1,249 @@
+// axis_pass.cu — one banded axis applied along rows or columns of planar
+// images, for geometries the fused separable kernel cannot tile (windows of
+// more than ~128-512 inputs per 16 outputs: large downscale factors, very
+// wide filters).  A resample then runs as two passes with a
+// bf16 intermediate in HBM (the same rounding point as the fused kernel's V):
+//
+//   vertical   mid[p][o][c] = Σ_k R[o][k] in[p][k][c]
+//              A = 16 input rows x 128 columns per K-step (TMA, MN-major,
+//              128B swizzle), B = the block's K x 16 weight tile,
+//              D (TMEM) lane = column, 16 outputs
+//   horizontal out[p][r][j] = Σ_k mid[p][r][k] C[j][k]
+//              A = 128 rows x 16 columns per K-step (TMA, K-major core
+//              matrices), B = the block's weight tile, D lane = row
+//
+// One CTA per (plane, 16-output block, 128-wide strip); the K window streams
+// through a 6-slot TMA ring with no upper bound on its length (windows up to
+// 1024 inputs, i.e. ~45x downscale).  Several CTAs share an SM (~40 KB smem,
+// 32 TMEM columns each).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "sm100.cuh"
+
+namespace tsb {
+
+ts_status encode_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* ptr,
+                         int64_t d0, int64_t d1, int64_t d2, int64_t stride1_elems,
+                         int64_t stride2_elems, int box0, int box1, CUtensorMapSwizzle swz);
+
+namespace apass {
+
+constexpr int kThreads = 128;
+constexpr int kRing = 6;
+constexpr uint32_t kStep = 4096;  // one K-step of A: 128 x 16 bf16
+
+struct Params {
+  AxisDev ax;
+  int planes, nb, nstrip;  // blocks along the axis, 128-wide strips across it
+  int nunits;
+};
+
+template <bool VERT, typename OutT>
+__global__ void __launch_bounds__(kThreads)
+    axis_pass_kernel(const __grid_constant__ CUtensorMap tm_in,
+                     const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ Params P) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_s = smem_u32(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_s - raw_s);
+  const uint32_t tile_bytes = static_cast<uint32_t>(P.ax.tile_bytes);
+  // [ring kRing x 4 KB][B tile][staging 128 x 16 x 4][barriers]
+  const uint32_t off_b = kRing * kStep;
+  const uint32_t off_out = off_b + ((tile_bytes + 1023u) & ~1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + off_out + 8192);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kRing;
+  uint64_t* wbar = bars + 2 * kRing;
+  uint64_t* done = wbar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int u = blockIdx.x;
+  const int strip = u % P.nstrip;
+  const int b = (u / P.nstrip) % P.nb;
+  const int p = u / (P.nstrip * P.nb);
+  const int32_t e = __ldg(P.ax.tab + b);
+  const int ws = e >> 16;          // window start (arithmetic shift keeps the sign)
+  const int tid = e & 0xFFFF;
+  const int nq = P.ax.K / 16;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(wbar, 1);
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<32>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(wbar, tile_bytes);
+      bulk_g2s(base + off_b, P.ax.tiles + static_cast<size_t>(tid) * tile_bytes, tile_bytes, wbar);
+      for (int q = 0; q < nq; ++q) {
+        const int s = q % kRing;
+        mbar_wait(&empty[s], ((q / kRing) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], kStep);
+        uint8_t* dst = base + s * kStep;
+        if (VERT) {  // rows ws+16q.., columns 128*strip.. as two 64-column boxes
+          tma_load_3d(dst, &tm_in, &full[s], 128 * strip, ws + 16 * q, p);
+          tma_load_3d(dst + 2048, &tm_in, &full[s], 128 * strip + 64, ws + 16 * q, p);
+        } else {     // rows 128*strip.., columns ws+16q.. as two 8-column boxes
+          tma_load_3d(dst, &tm_in, &full[s], ws + 16 * q, 128 * strip, p);
+          tma_load_3d(dst + 2048, &tm_in, &full[s], ws + 16 * q + 8, 128 * strip, p);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, VERT ? 1u : 0u, 0u);
+    const uint64_t bd0 = make_sdesc(base_s + off_b, 128u, static_cast<uint32_t>(P.ax.K) * 16u,
+                                    kSwizzleNone);
+    const uint64_t ad0 = VERT ? make_sdesc(base_s, 2048u, 1024u, kSwizzle128B)
+                              : make_sdesc(base_s, 2048u, 128u, kSwizzleNone);
+    mbar_wait(wbar, 0);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int q = 0; q < nq; ++q) {
+      mbar_wait(&full[s], ph);
+      __syncwarp();
+      tc_fence_after();
+      mma_f16_ss_elect(tmem, ad0 + static_cast<uint64_t>(s * (kStep >> 4)), bd0 + 16u * q, idesc,
+                       q > 0 ? 1u : 0u);
+      mma_commit_elect(&empty[s]);
+      if (++s == kRing) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    mma_commit_elect(done);
+  }
+  // epilogue: all four warps (lane = TMEM row)
+  mbar_wait(done, 0);
+  __syncwarp();  // reconverge warp 0 (lane 0 ran the producer loop)
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  uint32_t r[16];
+  tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16), r);
+  tmem_wait_ld();
+  OutT* stg = reinterpret_cast<OutT*>(base + off_out);
+  if (VERT) {  // lane = column c, values = 16 output rows: staging [16][128]
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float v = __uint_as_float(r[i]);
+      if constexpr (sizeof(OutT) == 2)
+        stg[i * 128 + row] = __float2bfloat16_rn(v);
+      else
+        stg[i * 128 + row] = v;
+    }
+  } else {     // lane = row r, values = 16 output columns: staging [128][16]
+    if constexpr (sizeof(OutT) == 2) {
+      uint32_t pk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+      uint4* d = reinterpret_cast<uint4*>(stg + row * 16);
+      d[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      d[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    } else {
+      uint4* d = reinterpret_cast<uint4*>(stg + row * 16);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) d[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (VERT)
+      tma_store_3d(&tm_out, stg, 128 * strip, 16 * b, p);
+    else
+      tma_store_3d(&tm_out, stg, 16 * b, 128 * strip, p);
+    bulk_commit();
+    bulk_wait0();
+  }
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<32>(tmem);
+  }
+}
+
+template <bool VERT, typename OutT>
+static cudaError_t launch(const Params& P, const CUtensorMap& tin, const CUtensorMap& tout,
+                          uint32_t smem, cudaStream_t stream) {
+  auto k = axis_pass_kernel<VERT, OutT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) k<<<P.nunits, kThreads, smem, stream>>>(tin, tout, P);
+  return e;
+}
+
+}  // namespace apass
+
+// Apply axis `a` along dimension `dim` (0: rows, 1: columns) of `planes`
+// planes: in (planes x H x W, bf16) -> out (rows: a->n_out x W; columns:
+// H x a->n_out), bf16 or f32.
+ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, const void* in,
+                        int64_t in_rs, int64_t in_ps, void* out, int64_t out_rs, int64_t out_ps,
+                        int out_dtype, cudaStream_t stream) {
+  if (!a || !in || !out || planes < 1 || H < 1 || W < 1 || (dim != 0 && dim != 1))
+    return set_error(TS_ERR_INVALID, "axis_pass: bad arguments");
+  if (out_dtype != TS_BF16 && out_dtype != TS_F32)
+    return set_error(TS_ERR_UNSUPPORTED, "axis_pass: output must be bf16 or f32");
+  const int n_in = dim == 0 ? H : W;
+  if (a->n_in != n_in)
+    return set_error(TS_ERR_INVALID, "axis_pass: axis expects %d inputs, image has %d", a->n_in,
+                     n_in);
+  const int oes = out_dtype == TS_BF16 ? 2 : 4;
+  const int OH = dim == 0 ? a->n_out : H, OW = dim == 0 ? W : a->n_out;
+  if (in_rs < W || (in_rs * 2) % 16 || in_ps < in_rs * H || (in_ps * 2) % 16 || out_rs < OW ||
+      (out_rs * oes) % 16 || out_ps < out_rs * OH || (out_ps * oes) % 16)
+    return set_error(TS_ERR_INVALID, "axis_pass: strides");
+  cudaError_t de = cudaSetDevice(a->device);
+  if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
+  apass::Params P;
+  P.ax = a->dev();
+  P.planes = planes;
+  P.nb = a->nb;
+  P.nstrip = ((dim == 0 ? W : H) + 127) / 128;
+  const int64_t units = static_cast<int64_t>(planes) * P.nb * P.nstrip;
+  if (units > 0x7FFFFFFF) return set_error(TS_ERR_UNSUPPORTED, "axis_pass: too many blocks");
+  P.nunits = static_cast<int>(units);
+  CUtensorMap tin, tout;
+  ts_status st;
+  if (dim == 0)
+    st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs, in_ps,
+                        64, 16, CU_TENSOR_MAP_SWIZZLE_128B);
+  else
+    st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs, in_ps,
+                        8, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st != TS_OK) return st;
+  const CUtensorMapDataType odt =
+      out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  st = encode_tmap_3d(&tout, odt, oes, out, OW, OH, planes, out_rs, out_ps, dim == 0 ? 128 : 16,
+                      dim == 0 ? 16 : 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st != TS_OK) return st;
+  const uint32_t smem = apass::kRing * apass::kStep +
+                        ((static_cast<uint32_t>(a->tile_bytes) + 1023u) & ~1023u) + 8192u + 256u +
+                        1024u;
+  cudaError_t e;
+  if (dim == 0)
+    e = out_dtype == TS_BF16
+            ? apass::launch<true, __nv_bfloat16>(P, tin, tout, smem, stream)
+            : apass::launch<true, float>(P, tin, tout, smem, stream);
+  else
+    e = out_dtype == TS_BF16
+            ? apass::launch<false, __nv_bfloat16>(P, tin, tout, smem, stream)
+            : apass::launch<false, float>(P, tin, tout, smem, stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "axis_pass launch");
+}
+
+}  // namespace tsb

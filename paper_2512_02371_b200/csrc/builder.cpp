@@ -147,11 +147,10 @@ static ts_status build_axis_host(int n_in, int n_out, int taps, const int32_t* f
     need = std::max(need, hi - ws[b] + 1);
   }
   const int K = round_up(need, 16);
-  if (K > 256)
+  if (K > kMaxWindow)
     return set_error(TS_ERR_UNSUPPORTED,
-                     "axis window %d exceeds 256 inputs per 16 outputs (scale too large for one "
-                     "block; split the resample into stages)",
-                     K);
+                     "axis window %d exceeds %d inputs per 16 outputs (scale too large)", K,
+                     kMaxWindow);
   a->K = K;
   a->tile_bytes = K * kBlockN * 2;
 

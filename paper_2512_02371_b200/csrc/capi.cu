@@ -18,6 +18,9 @@ ts_status separable_plan(const ts_axis* ra, const ts_axis* ca, int planes, int o
 void set_trace(void* buf, int ctas, int tiles);
 int separable_variant(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype);
 int strip_info(int* out16);
+ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, const void* in,
+                        int64_t in_rs, int64_t in_ps, void* out, int64_t out_rs, int64_t out_ps,
+                        int out_dtype, cudaStream_t stream);
 
 // ------------------------------------------------------------------ cast
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -165,6 +168,15 @@ ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes
 
 int ts_separable_variant(const ts_axis* rows, const ts_axis* cols, int planes, int out_dtype) {
   return separable_variant(rows, cols, planes, out_dtype);
+}
+
+ts_status ts_axis_pass(const ts_axis* a, int dim, int planes, int height, int width, const void* in,
+                       int64_t in_row_stride, int64_t in_plane_stride, void* out,
+                       int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
+                       void* stream) {
+  return axis_pass_run(a, dim, planes, height, width, in, in_row_stride, in_plane_stride, out,
+                       out_row_stride, out_plane_stride, out_dtype,
+                       static_cast<cudaStream_t>(stream));
 }
 
 int ts_strip_info(int* out16) { return out16 ? strip_info(out16) : 0; }

@@ -572,6 +572,10 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
   P.trace = g_trace;
   P.trace_ctas = g_trace_ctas;
   P.trace_tiles = g_trace_tiles;
+  if (ra->K > 256 || ca->K > 256)
+    return set_error(TS_ERR_UNSUPPORTED,
+                     "separable: windows %d / %d exceed the fused kernel's 256 (use axis passes)",
+                     ra->K, ca->K);
   if (ra->row_span > kMaxRowSpan || ra->row_span % 16)
     return set_error(TS_ERR_UNSUPPORTED, "rows axis: row tile span %d > %d", ra->row_span,
                      kMaxRowSpan);

@@ -55,6 +55,21 @@ def _as_planes_bf16(x, stream):
     return buf, Wp
 
 
+def fused_supported(ra, ca, planes=1, ts_out=None) -> bool:
+    """Whether the fused separable kernel tiles these axes (otherwise the
+    pipelines run two ``ts_axis_pass`` launches)."""
+    import ctypes
+    lib = _lib.load()
+    out8 = (ctypes.c_int * 8)()
+    st = lib.ts_separable_plan(ra.handle, ca.handle, planes, ts_out or _lib.TS_BF16, out8)
+    if st == 0:
+        return True
+    if st == 6:  # TS_ERR_UNSUPPORTED: geometry
+        return False
+    _lib.check(st, "ts_separable_plan")
+    return False
+
+
 def _run(x, ra, ca, out_dtype):
     torch = _torch()
     dev = _check_device(x)
@@ -71,9 +86,22 @@ def _run(x, ra, ca, out_dtype):
     owp = -(-ow // align) * align
     out = torch.empty((P, oh, owp), dtype=out_dtype, device=x.device)
     ts_out = _lib.TS_BF16 if out_dtype == torch.bfloat16 else _lib.TS_F32
-    _lib.check(_lib.load().ts_separable_run(
-        ra.handle, ca.handle, P, inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16,
-        out.data_ptr(), owp, owp * oh, ts_out, stream), "ts_separable_run")
+    lib = _lib.load()
+    if fused_supported(ra, ca, P, ts_out):
+        _lib.check(lib.ts_separable_run(
+            ra.handle, ca.handle, P, inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16,
+            out.data_ptr(), owp, owp * oh, ts_out, stream), "ts_separable_run")
+    else:
+        # windows too wide for the fused tile (large downscale factors, very
+        # wide filters): two axis passes, bf16 intermediate in HBM — the same
+        # rounding point as the fused kernel's intermediate
+        mid = torch.empty((P, oh, in_rs), dtype=torch.bfloat16, device=x.device)
+        _lib.check(lib.ts_axis_pass(ra.handle, 0, P, H, W, inb.data_ptr(), in_rs, in_rs * H,
+                                    mid.data_ptr(), in_rs, in_rs * oh, _lib.TS_BF16, stream),
+                   "ts_axis_pass")
+        _lib.check(lib.ts_axis_pass(ca.handle, 1, P, oh, W, mid.data_ptr(), in_rs, in_rs * oh,
+                                    out.data_ptr(), owp, owp * oh, ts_out, stream),
+                   "ts_axis_pass")
     if owp != ow:
         out = out[:, :, :ow]
     return out.reshape(*x.shape[:-2], oh, ow)

@@ -87,9 +87,12 @@ def test_builder_errors_map_to_reference_exceptions():
     spec = layout.ToeplitzSpec(l=4, k=8, p=2)
     with pytest.raises(errors.PhaseMismatch):
         axis.Axis.from_toeplitz(spec, np.ones(7, np.float32), 16, 8, device=-1)
-    first, w = filters.lanczos3_axis(2048, 143)  # 14x: one block needs > 256 inputs
+    first, w = filters.lanczos3_axis(4096, 64)  # 64x: one block needs > 1024 inputs
     with pytest.raises(errors.UnsupportedGeometry):
-        axis.Axis(2048, 143, first, w, device=-1)
+        axis.Axis(4096, 64, first, w, device=-1)
+    first, w = filters.lanczos3_axis(2048, 143)  # 14x: builds (runs as axis passes)
+    big = axis.Axis(2048, 143, first, w, device=-1)
+    assert big.info["window"] > 256
     with pytest.raises(errors.EvalError):
         axis.Axis(0, 4, np.zeros(4, np.int32), np.zeros((4, 2), np.float32), device=-1)
 

@@ -141,3 +141,48 @@ def test_upsample2x_matches_oracle(shape):
     ref = pipelines_ref.resample(x, 2 * H, 2 * W)
     assert y.shape == ref.shape
     assert np.abs(y - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("shape,oh,ow", [
+    ((3, 2160, 3840), 540, 960),   # 4x: rows window too wide for the fused tile
+    ((1, 2048, 2048), 143, 143),   # 14.3x
+    ((2, 300, 1000), 20, 40),      # 15x / 25x, ragged
+    ((1, 64, 2000), 64, 50),       # identity rows, 40x columns
+])
+def test_large_factor_resample_two_pass(shape, oh, ow):
+    """Scale factors whose windows exceed the fused kernel's tile run as two
+    ts_axis_pass launches; same oracle bound."""
+    import torch
+    from paper_2512_02371_b200 import axis, pipelines
+    ra = axis.lanczos3(shape[-2], oh, 0)
+    ca = axis.lanczos3(shape[-1], ow, 0)
+    assert not pipelines.fused_supported(ra, ca)
+    x = _img(shape, 21, smooth=shape[-1] >= 1000)
+    y = _gpu(pipelines.resample, x, out_h=oh, out_w=ow, out_dtype=torch.float32)
+    ref = pipelines_ref.resample(x, oh, ow)
+    assert y.shape == ref.shape == shape[:-2] + (oh, ow)
+    err = np.abs(y - ref).max()
+    assert err <= TOL, err
+
+
+def test_wide_gaussian_two_pass():
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = _img((2, 200, 328), 22)
+    y = _gpu(pipelines.gaussian_blur, x, taps=151, out_dtype=torch.float32)
+    ref = pipelines_ref.gaussian_blur(x, 151)
+    err = np.abs(y - ref).max()
+    assert err <= TOL, err
+
+
+def test_two_pass_matches_emulation():
+    """Two-pass path = fp32 emulation with a bf16 intermediate (the rounding
+    point of the fused kernel), up to f32 summation order."""
+    import torch
+    from paper_2512_02371_b200 import axis, pipelines
+    x = torch.from_numpy(_img((1, 1024, 1536), 23)).bfloat16().cuda()
+    y = pipelines.resample(x, 100, 96, out_dtype=torch.float32)
+    R = torch.as_tensor(axis.lanczos3(1024, 100, 0).dense(), device="cuda")
+    C = torch.as_tensor(axis.lanczos3(1536, 96, 0).dense(), device="cuda")
+    ref = (R @ x[0].float()).bfloat16().float() @ C.t()
+    assert (y[0] - ref).abs().max().item() <= 4e-3
