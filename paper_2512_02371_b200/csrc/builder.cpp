@@ -224,7 +224,7 @@ static ts_status build_axis_host(int n_in, int n_out, int taps, const int32_t* f
   // pass-2 (cols) geometry: as many blocks as fit a 128-column tile
   a->col_nbt = 0;
   a->col_span = 0;
-  for (int n = 8; n >= 1; --n) {
+  for (int n = kMaxColBlocks; n >= 1; --n) {
     int span = 0;
     for (int b0 = 0; b0 < nb; b0 += n) span = std::max(span, a->ws[b0 + n - 1] + K - a->ws[b0]);
     if (span <= kColTile) {

@@ -20,6 +20,7 @@ constexpr int kRowBlocksPerTile = 8;
 constexpr int kColTile = 128;
 // TMA boxes are at most 256 rows; a row tile is staged as two boxes
 constexpr int kMaxRowSpan = 512;
+constexpr int kMaxColBlocks = 16;  // pass-2 output blocks per tile (D_H: 256 TMEM columns)
 constexpr int kMaxWindow = 1024;  // inputs per 16-output block (axis_pass streams K)
 
 // Device-facing view of an axis (passed by value into kernels).

@@ -394,18 +394,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(dh_full, it & 1);
       if (warp == 6) trace_stamp(P, it, 8);
       tc_fence_after();
-      uint32_t r[8][16];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < nb2) tmem_ld16(t_lane + 16u * j, r[j]);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(dh_free);
       if (et == 0) bulk_wait_read0();  // previous TMA store finished reading staging
       named_bar_sync(2, 128);
+      // up to 16 blocks, 8 per batch of TMEM loads (128 registers)
+      for (int j0 = 0; j0 < nb2; j0 += 8) {
+        uint32_t r[8][16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < nb2) store_out_row<OutT>(orow + j * 16u * sizeof(OutT), r[j]);
+        for (int j = 0; j < 8; ++j)
+          if (j0 + j < nb2) tmem_ld16(t_lane + 16u * (j0 + j), r[j]);
+        tmem_wait_ld();
+        if (j0 + 8 >= nb2) {
+          tc_fence_before();
+          mbar_arrive(dh_free);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j0 + j < nb2) store_out_row<OutT>(orow + (j0 + j) * 16u * sizeof(OutT), r[j]);
+      }
       fence_proxy_async_smem();
       named_bar_sync(2, 128);
       if (et == 0) {
@@ -584,12 +589,9 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
                      ca->K);
   P.r = ra->dev();
   P.c = ca->dev();
-  P.nb2 = ca->col_nbt;
   P.R1 = ra->row_span;
   P.nrt = (ra->nb + kRowBlocksPerTile - 1) / kRowBlocksPerTile;
-  P.nct = (ca->nb + P.nb2 - 1) / P.nb2;
   P.planes = planes;
-  P.ntiles = planes * P.nrt * P.nct;
   const int ntr = static_cast<int>(ra->tab.size()), ntc = static_cast<int>(ca->tab.size());
   P.ptab = (ntr + ntc <= kParamTab) ? 1 : 0;
   P.ptab_c = ntr;
@@ -597,10 +599,14 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
     for (int i = 0; i < ntr; ++i) P.tab[i] = ra->tab[i];
     for (int i = 0; i < ntc; ++i) P.tab[ntr + i] = ca->tab[i];
   }
-  if (!plan_smem(P, oes))
-    return set_error(TS_ERR_UNSUPPORTED, "separable: tile (R1=%d, nb2=%d) does not fit smem",
-                     P.R1, P.nb2);
-  return TS_OK;
+  // widest column tile (most output blocks per staged V tile) that fits smem
+  for (int nb2 = ca->col_nbt; nb2 >= 1; --nb2) {
+    P.nb2 = nb2;
+    P.nct = (ca->nb + nb2 - 1) / nb2;
+    P.ntiles = planes * P.nrt * P.nct;
+    if (plan_smem(P, oes)) return TS_OK;
+  }
+  return set_error(TS_ERR_UNSUPPORTED, "separable: tile (R1=%d) does not fit smem", P.R1);
 }
 
 ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const void* in,
