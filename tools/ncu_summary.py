@@ -1,6 +1,8 @@
 """Summarise an ncu report (--set full) and a launch list into profiles/.
 
-    python tools/ncu_summary.py REPORT.ncu-rep LAUNCHES.csv OUT_PREFIX [frames]
+    python tools/ncu_summary.py REPORT.ncu-rep LAUNCHES.csv|- OUT_PREFIX [frames] [alg_bytes_per_frame]
+
+(the default algorithmic bytes per frame are config c2's: 4K RGB bf16 in, 1080p bf16 out)
 """
 import csv
 import io
@@ -57,14 +59,15 @@ def main():
     dur_us = float(k["gpu__time_duration.sum"][0])
     rd = to_bytes(*k["dram__bytes_read.sum"])
     wr = to_bytes(*k["dram__bytes_write.sum"])
-    alg = frames * (3 * 2160 * 3840 * 2 + 3 * 1080 * 1920 * 2)
+    per_frame = int(sys.argv[5]) if len(sys.argv) > 5 else 3 * 2160 * 3840 * 2 + 3 * 1080 * 1920 * 2
+    alg = frames * per_frame
     summary = {
         "kernel": k["Kernel Name"][0][:120],
         "frames": frames,
         "duration_us": dur_us,
         "dram_read_bytes": rd, "dram_write_bytes": wr,
         "dram_bytes_per_frame": (rd + wr) / frames,
-        "alg_bytes": alg, "traffic_over_alg": (rd + wr) / alg,
+        "alg_bytes": alg, "alg_bytes_per_frame": per_frame, "traffic_over_alg": (rd + wr) / alg,
         "achieved_alg_GBps": alg / dur_us / 1e3,
         "metrics": {h: " ".join(v) for h, v in k.items() if h != "Kernel Name"},
         "launch_list": launches(lcsv) if lcsv != "-" else None,
