@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <string>
+#include <atomic>
 #include <vector>
 
 #include "../../include/tensorsel_b200.h"
@@ -62,7 +63,17 @@ struct StripPlan {
 };
 }  // namespace tsb
 
+namespace tsb {
+// process-unique axis id (launch-parameter caches key on it, never on the
+// pointer, which the allocator may reuse)
+inline uint64_t next_axis_uid() {
+  static std::atomic<uint64_t> n{1};
+  return n.fetch_add(1);
+}
+}  // namespace tsb
+
 struct ts_axis {
+  uint64_t uid = tsb::next_axis_uid();
   int n_in = 0, n_out = 0, taps = 0;
   int K = 0, nb = 0, ntiles = 0, tile_bytes = 0;
   int row_span = 0;            // rows staged per pass-1 tile (multiple of 16)

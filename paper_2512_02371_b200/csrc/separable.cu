@@ -475,10 +475,15 @@ ts_status encode_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, cons
 }
 
 int sm_count_current() {
-  int dev = 0, n = 0;
+  static int cache[64] = {0};
+  int dev = 0;
   cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && cache[dev] > 0) return cache[dev];
+  int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
+  n = n > 0 ? n : 148;
+  if (dev >= 0 && dev < 64) cache[dev] = n;
+  return n;
 }
 
 // Pick stages / V buffers / weight residency to fit the shared-memory budget,
@@ -521,10 +526,17 @@ template <typename OutT, int KQ1, int KQ2>
 static ts_status launch_sep_k(const SepParams& P, const CUtensorMap& tin, const CUtensorMap& tout,
                               cudaStream_t stream) {
   auto kern = separable_kernel<OutT, KQ1, KQ2>;
-  // per-device attribute; cheap, so set it on every launch
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(P.L.total));
-  if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(separable smem)");
+  // the smem ceiling is set once per device (to the maximum any plan uses)
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = cudaSuccess;
+  if (dev < 0 || dev >= 64 || !attr_done[dev]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmemLimit));
+    if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(separable smem)");
+    if (dev >= 0 && dev < 64) attr_done[dev] = true;
+  }
   const int sms = sm_count_current();
   const int grid = P.ntiles < sms ? P.ntiles : sms;
   kern<<<grid, kThreads, P.L.total, stream>>>(tin, tout, P);
@@ -637,9 +649,35 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
                            stream, false);
   if (s5 != TS_ERR_UNSUPPORTED) return s5;
 
-  SepParams P;
-  ts_status st = make_params(ra, ca, planes, oes, P);
-  if (st != TS_OK) return st;
+  // launch parameters (block tables, smem plan) are cached per (axes, planes,
+  // output size): rebuilding them costs more host time than a 1-frame launch
+  struct Cached {
+    uint64_t ru = 0, cu = 0;
+    int planes = 0, oes = 0;
+    SepParams P;
+  };
+  static thread_local Cached cache[4];
+  static thread_local int cache_next = 0;
+  Cached* hit = nullptr;
+  for (auto& c : cache)
+    if (c.ru == ra->uid && c.cu == ca->uid && c.planes == planes && c.oes == oes) hit = &c;
+  if (!hit) {
+    Cached& c = cache[cache_next];
+    cache_next = (cache_next + 1) % 4;
+    c.ru = 0;
+    ts_status st = make_params(ra, ca, planes, oes, c.P);
+    if (st != TS_OK) return st;
+    c.ru = ra->uid;
+    c.cu = ca->uid;
+    c.planes = planes;
+    c.oes = oes;
+    hit = &c;
+  }
+  SepParams& P = hit->P;
+  P.trace = g_trace;
+  P.trace_ctas = g_trace_ctas;
+  P.trace_tiles = g_trace_tiles;
+  ts_status st;
   CUtensorMap tin, tout;
   st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, ca->n_in, ra->n_in, planes,
                       in_rs, in_ps, 64, P.R1 / 2, CU_TENSOR_MAP_SWIZZLE_128B);

@@ -17,6 +17,8 @@ no CPU path: without the native library or a CUDA device these raise.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 from . import _lib, axis as _axis, filters
@@ -39,7 +41,7 @@ def _as_planes_bf16(x, stream):
     """View/copy x (..., H, W) as a (P, H, Wp) bf16 buffer with Wp % 8 == 0."""
     torch = _torch()
     H, W = x.shape[-2], x.shape[-1]
-    P = int(np.prod(x.shape[:-2])) if x.dim() > 2 else 1
+    P = math.prod(x.shape[:-2]) if x.dim() > 2 else 1
     if x.dtype == torch.bfloat16 and W % 8 == 0 and x.is_contiguous():
         return x.reshape(P, H, W), W
     Wp = -(-W // 8) * 8
@@ -55,25 +57,39 @@ def _as_planes_bf16(x, stream):
     return buf, Wp
 
 
+_FUSED = {}
+
+
 def fused_supported(ra, ca, planes=1, ts_out=None) -> bool:
     """Whether the fused separable kernel tiles these axes (otherwise the
-    pipelines run two ``ts_axis_pass`` launches)."""
+    pipelines run two ``ts_axis_pass`` launches).  Memoised per axis pair."""
+    key = (ra, ca, planes, ts_out or _lib.TS_BF16)
+    ok = _FUSED.get(key)
+    if ok is not None:
+        return ok
     import ctypes
     lib = _lib.load()
     out8 = (ctypes.c_int * 8)()
-    st = lib.ts_separable_plan(ra.handle, ca.handle, planes, ts_out or _lib.TS_BF16, out8)
-    if st == 0:
-        return True
-    if st == 6:  # TS_ERR_UNSUPPORTED: geometry
-        return False
-    _lib.check(st, "ts_separable_plan")
-    return False
+    st = lib.ts_separable_plan(ra.handle, ca.handle, planes, key[3], out8)
+    if st not in (0, 6):  # 6 = TS_ERR_UNSUPPORTED: geometry
+        _lib.check(st, "ts_separable_plan")
+    _FUSED[key] = ok = st == 0
+    return ok
+
+
+def _stream(x):
+    """Raw cudaStream_t of the current stream on x's device."""
+    torch = _torch()
+    get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if get is not None:
+        return get(x.device.index if x.device.index is not None else torch.cuda.current_device())
+    return torch.cuda.current_stream(x.device).cuda_stream
 
 
 def _run(x, ra, ca, out_dtype):
     torch = _torch()
-    dev = _check_device(x)
-    stream = torch.cuda.current_stream(x.device).cuda_stream
+    _check_device(x)
+    stream = _stream(x)
     H, W = x.shape[-2], x.shape[-1]
     if ra.n_in != H or ca.n_in != W:
         raise ValueError(f"axes expect {ra.n_in} x {ca.n_in}, image is {H} x {W}")
@@ -172,7 +188,7 @@ def denoise_dct16(x, threshold: float = 0.15, mode: str = "hard", *, out_dtype=N
     _check_device(x)
     if mode not in ("hard", "soft"):
         raise ValueError("mode must be 'hard' or 'soft'")
-    stream = torch.cuda.current_stream(x.device).cuda_stream
+    stream = _stream(x)
     H, W = x.shape[-2], x.shape[-1]
     out_dtype = out_dtype or (x.dtype if x.dtype in (torch.bfloat16, torch.float32)
                               else torch.bfloat16)
