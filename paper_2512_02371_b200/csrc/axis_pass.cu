@@ -12,13 +12,16 @@
 //              A = 128 rows x 16 columns per K-step (TMA, K-major core
 //              matrices), B = the block's weight tile, D lane = row
 //
-// One CTA per (plane, 16-output block, 128-wide strip); the K window streams
-// through a 6-slot TMA ring with no upper bound on its length (windows up to
-// 1024 inputs, i.e. ~45x downscale).  Several CTAs share an SM (~40 KB smem,
-// 32 TMEM columns each).
+// One CTA per (plane, group of up to 8 16-output blocks, 128-wide strip);
+// each block's K window streams through an 8-slot TMA ring with no upper
+// bound on its length (windows up to 1024 inputs, i.e. ~45x downscale), the
+// blocks accumulate into adjacent 16-column TMEM slices and leave in one TMA
+// store.  Two CTAs share an SM (<= ~104 KB smem, 128 TMEM columns each).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "common.h"
 #include "sm100.cuh"
@@ -38,7 +41,9 @@ constexpr uint32_t kStep = 4096;  // one K-step of A: 128 x 16 bf16
 struct Params {
   AxisDev ax;
   int planes, nb, nstrip;  // blocks along the axis, 128-wide strips across it
+  int nbg, ngroups;        // blocks per CTA (<= 8) and block groups
   int nunits;
+  uint32_t off_b, off_out, off_bar;
 };
 
 template <bool VERT, typename OutT>
@@ -50,10 +55,8 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_s - raw_s);
   const uint32_t tile_bytes = static_cast<uint32_t>(P.ax.tile_bytes);
-  // [ring kRing x 4 KB][B tile][staging 128 x 16 x 4][barriers]
-  const uint32_t off_b = kRing * kStep;
-  const uint32_t off_out = off_b + ((tile_bytes + 1023u) & ~1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + off_out + 8192);
+  // [ring kRing x 4 KB][B tiles of the group][staging][barriers]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + P.off_bar);
   uint64_t* full = bars;
   uint64_t* empty = bars + kRing;
   uint64_t* wbar = bars + 2 * kRing;
@@ -63,11 +66,10 @@ __global__ void __launch_bounds__(kThreads)
 
   const int u = blockIdx.x;
   const int strip = u % P.nstrip;
-  const int b = (u / P.nstrip) % P.nb;
-  const int p = u / (P.nstrip * P.nb);
-  const int32_t e = __ldg(P.ax.tab + b);
-  const int ws = e >> 16;          // window start (arithmetic shift keeps the sign)
-  const int tid = e & 0xFFFF;
+  const int g = (u / P.nstrip) % P.ngroups;
+  const int p = u / (P.nstrip * P.ngroups);
+  const int b0 = g * P.nbg;
+  const int nblk = min(P.nbg, P.nb - b0);
   const int nq = P.ax.K / 16;
 
   if (threadIdx.x == 0) {
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(kThreads)
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<32>(tmem_slot);
+  if (warp == 1) tmem_alloc<128>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -87,41 +89,56 @@ __global__ void __launch_bounds__(kThreads)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(wbar, tile_bytes);
-      bulk_g2s(base + off_b, P.ax.tiles + static_cast<size_t>(tid) * tile_bytes, tile_bytes, wbar);
-      for (int q = 0; q < nq; ++q) {
-        const int s = q % kRing;
-        mbar_wait(&empty[s], ((q / kRing) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[s], kStep);
-        uint8_t* dst = base + s * kStep;
-        if (VERT) {  // rows ws+16q.., columns 128*strip.. as two 64-column boxes
-          tma_load_3d(dst, &tm_in, &full[s], 128 * strip, ws + 16 * q, p);
-          tma_load_3d(dst + 2048, &tm_in, &full[s], 128 * strip + 64, ws + 16 * q, p);
-        } else {     // rows 128*strip.., columns ws+16q.. as two 8-column boxes
-          tma_load_3d(dst, &tm_in, &full[s], ws + 16 * q, 128 * strip, p);
-          tma_load_3d(dst + 2048, &tm_in, &full[s], ws + 16 * q + 8, 128 * strip, p);
+      mbar_arrive_expect_tx(wbar, tile_bytes * nblk);
+      for (int j = 0; j < nblk; ++j) {
+        const int tid = __ldg(P.ax.tab + b0 + j) & 0xFFFF;
+        bulk_g2s(base + P.off_b + j * tile_bytes, P.ax.tiles + static_cast<size_t>(tid) * tile_bytes,
+                 tile_bytes, wbar);
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      for (int j = 0; j < nblk; ++j) {
+        const int ws = __ldg(P.ax.tab + b0 + j) >> 16;  // window start (signed)
+        for (int q = 0; q < nq; ++q) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], kStep);
+          uint8_t* dst = base + s * kStep;
+          if (VERT) {  // rows ws+16q.., columns 128*strip.. as two 64-column boxes
+            tma_load_3d(dst, &tm_in, &full[s], 128 * strip, ws + 16 * q, p);
+            tma_load_3d(dst + 2048, &tm_in, &full[s], 128 * strip + 64, ws + 16 * q, p);
+          } else {     // rows 128*strip.., columns ws+16q.. as two 8-column boxes
+            tma_load_3d(dst, &tm_in, &full[s], ws + 16 * q, 128 * strip, p);
+            tma_load_3d(dst + 2048, &tm_in, &full[s], ws + 16 * q + 8, 128 * strip, p);
+          }
+          if (++s == kRing) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, VERT ? 1u : 0u, 0u);
-    const uint64_t bd0 = make_sdesc(base_s + off_b, 128u, static_cast<uint32_t>(P.ax.K) * 16u,
+    const uint64_t bd0 = make_sdesc(base_s + P.off_b, 128u, static_cast<uint32_t>(P.ax.K) * 16u,
                                     kSwizzleNone);
     const uint64_t ad0 = VERT ? make_sdesc(base_s, 2048u, 1024u, kSwizzle128B)
                               : make_sdesc(base_s, 2048u, 128u, kSwizzleNone);
     mbar_wait(wbar, 0);
     int s = 0;
     uint32_t ph = 0;
-    for (int q = 0; q < nq; ++q) {
-      mbar_wait(&full[s], ph);
-      __syncwarp();
-      tc_fence_after();
-      mma_f16_ss_elect(tmem, ad0 + static_cast<uint64_t>(s * (kStep >> 4)), bd0 + 16u * q, idesc,
-                       q > 0 ? 1u : 0u);
-      mma_commit_elect(&empty[s]);
-      if (++s == kRing) {
-        s = 0;
-        ph ^= 1;
+    for (int j = 0; j < nblk; ++j) {
+      const uint64_t bdj = bd0 + static_cast<uint64_t>(j * (tile_bytes >> 4));
+      for (int q = 0; q < nq; ++q) {
+        mbar_wait(&full[s], ph);
+        __syncwarp();
+        tc_fence_after();
+        mma_f16_ss_elect(tmem + 16u * j, ad0 + static_cast<uint64_t>(s * (kStep >> 4)),
+                         bdj + 16u * q, idesc, q > 0 ? 1u : 0u);
+        mma_commit_elect(&empty[s]);
+        if (++s == kRing) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
     mma_commit_elect(done);
@@ -131,48 +148,55 @@ __global__ void __launch_bounds__(kThreads)
   __syncwarp();  // reconverge warp 0 (lane 0 ran the producer loop)
   tc_fence_after();
   const int row = warp * 32 + lane;
-  uint32_t r[16];
-  tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16), r);
-  tmem_wait_ld();
-  OutT* stg = reinterpret_cast<OutT*>(base + off_out);
-  if (VERT) {  // lane = column c, values = 16 output rows: staging [16][128]
+  const uint32_t tl = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  OutT* stg = reinterpret_cast<OutT*>(base + P.off_out);
+#pragma unroll 1
+  for (int j = 0; j < nblk; ++j) {
+    uint32_t r[16];
+    tmem_ld16(tl + 16u * j, r);
+    tmem_wait_ld();
+    if (VERT) {  // lane = column c, values = 16 output rows: staging [nout][128]
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float v = __uint_as_float(r[i]);
-      if constexpr (sizeof(OutT) == 2)
-        stg[i * 128 + row] = __float2bfloat16_rn(v);
-      else
-        stg[i * 128 + row] = v;
-    }
-  } else {     // lane = row r, values = 16 output columns: staging [128][16]
-    if constexpr (sizeof(OutT) == 2) {
-      uint32_t pk[8];
+      for (int i = 0; i < 16; ++i) {
+        const float v = __uint_as_float(r[i]);
+        if constexpr (sizeof(OutT) == 2)
+          stg[(16 * j + i) * 128 + row] = __float2bfloat16_rn(v);
+        else
+          stg[(16 * j + i) * 128 + row] = v;
+      }
+    } else {     // lane = row r, values = 16 output columns: staging [128][nout]
+      OutT* d = stg + row * (16 * P.nbg) + 16 * j;  // box row pitch: nbg blocks
+      if constexpr (sizeof(OutT) == 2) {
+        uint32_t pk[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-      uint4* d = reinterpret_cast<uint4*>(stg + row * 16);
-      d[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      d[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-    } else {
-      uint4* d = reinterpret_cast<uint4*>(stg + row * 16);
+        for (int i = 0; i < 8; ++i)
+          pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+        uint4* d4 = reinterpret_cast<uint4*>(d);
+        d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      } else {
+        uint4* d4 = reinterpret_cast<uint4*>(d);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) d[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+        for (int i = 0; i < 4; ++i)
+          d4[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+      }
     }
   }
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) {
+    // the box covers nbg blocks; a short last group is clipped by the axis end
     if (VERT)
-      tma_store_3d(&tm_out, stg, 128 * strip, 16 * b, p);
+      tma_store_3d(&tm_out, stg, 128 * strip, 16 * b0, p);
     else
-      tma_store_3d(&tm_out, stg, 16 * b, 128 * strip, p);
+      tma_store_3d(&tm_out, stg, 16 * b0, 128 * strip, p);
     bulk_commit();
     bulk_wait0();
   }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<32>(tmem);
+    tmem_dealloc<128>(tmem);
   }
 }
 
@@ -213,9 +237,24 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   P.planes = planes;
   P.nb = a->nb;
   P.nstrip = ((dim == 0 ? W : H) + 127) / 128;
-  const int64_t units = static_cast<int64_t>(planes) * P.nb * P.nstrip;
+  // blocks per CTA: more blocks amortise the per-CTA setup, fewer keep more
+  // CTAs (and so more 2 KB TMA boxes) in flight per SM, which is what the
+  // load path needs — group only when there are plenty of units
+  const uint32_t tb = static_cast<uint32_t>(a->tile_bytes);
+  const int64_t base_units = static_cast<int64_t>(planes) * a->nb * P.nstrip;
+  P.nbg = 1;
+  while (P.nbg < 8 && base_units / (2 * P.nbg) >= 148 * 64 && (2u * P.nbg) * tb <= 32768u)
+    P.nbg *= 2;
+  if (const char* f = std::getenv("TSB_APASS_NBG")) P.nbg = std::atoi(f) > 0 ? std::atoi(f) : 1;
+  if (P.nbg > P.nb) P.nbg = P.nb;
+  P.ngroups = (P.nb + P.nbg - 1) / P.nbg;
+  const int64_t units = static_cast<int64_t>(planes) * P.ngroups * P.nstrip;
   if (units > 0x7FFFFFFF) return set_error(TS_ERR_UNSUPPORTED, "axis_pass: too many blocks");
   P.nunits = static_cast<int>(units);
+  P.off_b = apass::kRing * apass::kStep;
+  P.off_out = P.off_b + ((static_cast<uint32_t>(P.nbg) * tb + 1023u) & ~1023u);
+  P.off_bar = P.off_out + ((128u * 16u * P.nbg * oes + 1023u) & ~1023u);
+  const uint32_t smem = P.off_bar + 256u + 1024u;
   CUtensorMap tin, tout;
   ts_status st;
   if (dim == 0)
@@ -227,12 +266,10 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   if (st != TS_OK) return st;
   const CUtensorMapDataType odt =
       out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  st = encode_tmap_3d(&tout, odt, oes, out, OW, OH, planes, out_rs, out_ps, dim == 0 ? 128 : 16,
-                      dim == 0 ? 16 : 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+  st = encode_tmap_3d(&tout, odt, oes, out, OW, OH, planes, out_rs, out_ps,
+                      dim == 0 ? 128 : 16 * P.nbg, dim == 0 ? 16 * P.nbg : 128,
+                      CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TS_OK) return st;
-  const uint32_t smem = apass::kRing * apass::kStep +
-                        ((static_cast<uint32_t>(a->tile_bytes) + 1023u) & ~1023u) + 8192u + 256u +
-                        1024u;
   cudaError_t e;
   if (dim == 0)
     e = out_dtype == TS_BF16

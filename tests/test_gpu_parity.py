@@ -145,7 +145,9 @@ def test_upsample2x_matches_oracle(shape):
 
 @pytest.mark.parametrize("shape,oh,ow", [
     ((3, 2160, 3840), 540, 960),   # 4x: rows window too wide for the fused tile
-    ((1, 2048, 2048), 143, 143),   # 14.3x
+    ((1, 2048, 2048), 143, 143),   # the paper's 2048^2 table
+    ((1, 2048, 2048), 245, 245),
+    ((1, 2048, 2048), 450, 450),
     ((2, 300, 1000), 20, 40),      # 15x / 25x, ragged
     ((1, 64, 2000), 64, 50),       # identity rows, 40x columns
 ])
@@ -186,3 +188,13 @@ def test_two_pass_matches_emulation():
     C = torch.as_tensor(axis.lanczos3(1536, 96, 0).dense(), device="cuda")
     ref = (R @ x[0].float()).bfloat16().float() @ C.t()
     assert (y[0] - ref).abs().max().item() <= 4e-3
+
+
+def test_paper_table_921():
+    """2048^2 -> 921^2 (2.22x), the last row of the paper's table."""
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = _img((1, 2048, 2048), 24)
+    y = _gpu(pipelines.resample, x, out_h=921, out_w=921, out_dtype=torch.float32)
+    ref = pipelines_ref.resample(x, 921, 921)
+    assert np.abs(y - ref).max() <= TOL
