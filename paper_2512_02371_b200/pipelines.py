@@ -95,9 +95,11 @@ def _run(x, ra, ca, out_dtype):
         raise ValueError(f"axes expect {ra.n_in} x {ca.n_in}, image is {H} x {W}")
     out_dtype = out_dtype or (x.dtype if x.dtype in (torch.bfloat16, torch.float32)
                               else torch.bfloat16)
+    oh, ow = ra.n_out, ca.n_out
+    if x.numel() == 0:  # empty batch: nothing to launch
+        return torch.empty((*x.shape[:-2], oh, ow), dtype=out_dtype, device=x.device)
     inb, in_rs = _as_planes_bf16(x, stream)
     P = inb.shape[0]
-    oh, ow = ra.n_out, ca.n_out
     align = 8 if out_dtype == torch.bfloat16 else 4
     owp = -(-ow // align) * align
     out = torch.empty((P, oh, owp), dtype=out_dtype, device=x.device)
@@ -192,6 +194,8 @@ def denoise_dct16(x, threshold: float = 0.15, mode: str = "hard", *, out_dtype=N
     H, W = x.shape[-2], x.shape[-1]
     out_dtype = out_dtype or (x.dtype if x.dtype in (torch.bfloat16, torch.float32)
                               else torch.bfloat16)
+    if x.numel() == 0:
+        return torch.empty(x.shape, dtype=out_dtype, device=x.device)
     inb, in_rs = _as_planes_bf16(x, stream)
     P = inb.shape[0]
     align = 8 if out_dtype == torch.bfloat16 else 4

@@ -1,0 +1,83 @@
+"""Edge cases of the GPU pipelines against the CPU oracle: empty batches,
+tiny and ragged images, degenerate kernels, batched leading dims."""
+
+import numpy as np
+import pytest
+
+from oracle import pipelines_ref
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+
+def _img(shape, seed):
+    import torch
+    x = np.random.default_rng(seed).random(shape, dtype=np.float32)
+    return torch.from_numpy(x).bfloat16().float().numpy()
+
+
+def _gpu(fn, x, **kw):
+    import torch
+    y = fn(torch.from_numpy(x).bfloat16().cuda(), out_dtype=torch.float32, **kw)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def test_empty_batch_returns_empty():
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = torch.empty((0, 3, 64, 64), dtype=torch.bfloat16, device="cuda")
+    assert pipelines.resample(x, 32, 32).shape == (0, 3, 32, 32)
+    assert pipelines.gaussian_blur(x, 9).shape == (0, 3, 64, 64)
+    assert pipelines.denoise_dct16(x, 0.1).shape == (0, 3, 64, 64)
+
+
+@pytest.mark.parametrize("shape,oh,ow", [
+    ((1, 1, 1), 1, 1), ((1, 1, 7), 1, 3), ((2, 3, 5), 6, 10), ((1, 9, 1), 4, 1),
+    ((1, 17, 33), 8, 16),
+])
+def test_tiny_and_ragged_resample(shape, oh, ow):
+    from paper_2512_02371_b200 import pipelines
+    x = _img(shape, 31)
+    y = _gpu(pipelines.resample, x, out_h=oh, out_w=ow)
+    ref = pipelines_ref.resample(x, oh, ow)
+    assert y.shape == ref.shape
+    assert np.abs(y - ref).max() <= TOL
+
+
+def test_batched_leading_dims_match_flat():
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = torch.from_numpy(_img((2, 3, 3, 48, 80), 32)).bfloat16().cuda()
+    y = pipelines.downsample2x(x, out_dtype=torch.float32)
+    yf = pipelines.downsample2x(x.reshape(18, 48, 80), out_dtype=torch.float32)
+    assert y.shape == (2, 3, 3, 24, 40)
+    assert torch.equal(y.reshape(18, 24, 40), yf)
+
+
+@pytest.mark.parametrize("taps", [1, 3])
+def test_degenerate_gaussian(taps):
+    from paper_2512_02371_b200 import pipelines
+    x = _img((1, 40, 56), 33)
+    y = _gpu(pipelines.gaussian_blur, x, taps=taps)
+    ref = pipelines_ref.gaussian_blur(x, taps)
+    assert np.abs(y - ref).max() <= TOL
+    if taps == 1:
+        assert np.abs(y - x).max() <= 4e-3  # identity up to bf16 rounding
+
+
+@pytest.mark.parametrize("shape", [(1, 8, 8), (1, 8, 24), (2, 40, 8), (1, 120, 232)])
+def test_dct_small_and_band_edge_sizes(shape):
+    from paper_2512_02371_b200 import pipelines
+    x = _img(shape, 34)
+    y = _gpu(pipelines.denoise_dct16, x, threshold=0.15, mode="soft")
+    ref = pipelines_ref.dct_denoise(x, 0.15, "soft")
+    assert np.abs(y - ref).max() <= TOL
+
+
+def test_f32_output_odd_width():
+    from paper_2512_02371_b200 import pipelines
+    x = _img((3, 50, 77), 35)
+    y = _gpu(pipelines.resample, x, out_h=25, out_w=39)
+    ref = pipelines_ref.resample(x, 25, 39)
+    assert np.abs(y - ref).max() <= TOL
