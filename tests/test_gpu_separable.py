@@ -147,3 +147,4 @@ def test_strip_variant_selection(monkeypatch):
     assert _variant(*odd, 3) == 4
     k = filters.gaussian_taps(9)
     assert _variant(axis.convolution(512, k, 0), axis.convolution(1024, k, 0)) == 5
+
