@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.h"
@@ -64,12 +65,12 @@ constexpr uint32_t kOffOut = kOffB7 + 2 * 32768;         // 112 x 112 staging (f
 constexpr uint32_t kOutBytes = kOut * kOut * 4;
 constexpr uint32_t kOffC = kOffOut + ((kOutBytes + 1023) / 1024) * 1024;
 // constants (built on the host, one bulk copy per CTA):
-//   S1 strips: [p][hi/lo] 240 rows x 16 K, K-major core matrices (7680 B each)
+//   S1 strip : hi, lo: 240 rows x 16 K, K-major core matrices (7680 B each)
 //   S7 strip : 248 rows x 16 K
 //   B3       : Dwᵀ as the S3 B operand (K = sample, N = freq), hi + lo
 //   B5       : Dw f32 (K = freq, N = sample) for S5
 constexpr uint32_t kStripBytes = 7680;
-constexpr uint32_t kCS7 = 4 * kStripBytes;
+constexpr uint32_t kCS7 = 2 * kStripBytes;
 constexpr uint32_t kCB3 = kCS7 + 7936;
 constexpr uint32_t kCB5 = kCB3 + 1024;
 constexpr uint32_t kConstBytes = kCB5 + 1024;
@@ -91,7 +92,8 @@ struct Params {
   int trace_ctas, trace_tiles;
 };
 
-// events: 12p + {0 D1 seen, 1 C1 done, 2 D2 seen, 3 E2 done, 4 D3 seen, 5 E3 done};
+// events: 12p + {0 D1 seen, 1 C1 done, 2 D2 (q=0) seen, 6 D2 (q=1) seen, 3 E2 done,
+// 4 D3 seen, 5 E3 done};
 // 7 MMA: band ready, 8 MMA: S1 issued (p=0); 22 E4 start, 23 E4 stored
 __device__ __forceinline__ void stamp(const Params& P, int it, int ev) {
   if (P.trace != nullptr && static_cast<int>(blockIdx.x) < P.trace_ctas && it < P.trace_tiles)
@@ -212,14 +214,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* xready = bars + 4;   // [2]
   uint64_t* s1done = bars + 6;
   uint64_t* c1 = bars + 7;
-  uint64_t* s3done = bars + 8;
-  uint64_t* e2 = bars + 9;
-  uint64_t* s5done = bars + 10;
-  uint64_t* e3 = bars + 11;
-  uint64_t* s7done = bars + 12;
-  uint64_t* e4 = bars + 13;
-  uint64_t* cbar = bars + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* s3done = bars + 8;   // [2]: column phase q = 0 / 1 tiles done
+  uint64_t* e2 = bars + 10;      // [2]: their coefficients cored
+  uint64_t* s5done = bars + 12;
+  uint64_t* e3 = bars + 13;
+  uint64_t* s7done = bars + 14;
+  uint64_t* e4 = bars + 15;
+  uint64_t* cbar = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -229,11 +231,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&xready[s], 1);
     }
     mbar_init(s1done, 1);
-    mbar_init(s3done, 1);
+    mbar_init(&s3done[0], 1);
+    mbar_init(&s3done[1], 1);
     mbar_init(s5done, 1);
     mbar_init(s7done, 1);
     mbar_init(c1, kEpiThreads);
-    mbar_init(e2, kEpiThreads);
+    mbar_init(&e2[0], kEpiThreads);
+    mbar_init(&e2[1], kEpiThreads);
     mbar_init(e3, kEpiThreads);
     mbar_init(e4, kEpiThreads);
     mbar_init(cbar, 1);
@@ -284,29 +288,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t b5 = make_sdesc(base_s + kOffC + kCB5, 128u, 512u, kSwizzleNone);
     const uint64_t b7 = make_sdesc(base_s + kOffB7, 16384u, 1024u, kSwizzle128B);
     mbar_wait(cbar, 0);
+    // S1: D1 = T_p · X, 8 (p = 0) or 7 (p = 1) K-steps of 16 band rows, A
+    // strip hi + lo.  Row phase 1 reuses the phase-0 strip with the band
+    // descriptor moved down 8 rows (one 1 KB swizzle atom): its tiles then
+    // start on K-step boundaries.
+    auto issue_s1 = [&](int s, int p) {
+      const uint64_t bx =
+          make_sdesc(base_s + kOffX + s * kBandBytes + p * 1024u, 16384u, 1024u, kSwizzle128B);
+      tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (p == 1 && k == 7) break;
+        const uint32_t so = (14u - 2u * k) * 16u;  // strip offset, 16-byte units
+        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + so), bx + 128u * k, id128, k > 0 ? 1u : 0u);
+        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + kStripBytes / 16 + so), bx + 128u * k, id128,
+                         1u);
+      }
+      mma_commit_elect(s1done);  // before any later S7: C1 must not wait for it
+      if (p == 1) mma_commit_elect(&xempty[s]);
+    };
     int it = 0;
     uint32_t ph = 0;  // phase of the per-row-phase barriers (two completions per band)
-    for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
+    int t = blockIdx.x;
+    if (t < P.nregions) {
+      mbar_wait(&xfull[0], 0);
+      mbar_wait(&xready[0], 0);
+      if (lane == 0) stamp(P, 0, 7);
+      issue_s1(0, 0);
+    }
+    for (; t < P.nregions; t += gridDim.x, ++it) {
       const int s = it & 1;
-      mbar_wait(&xfull[s], (it >> 1) & 1);
-      mbar_wait(&xready[s], (it >> 1) & 1);
-      if (lane == 0) stamp(P, it, 7);
-      const uint64_t bx = make_sdesc(base_s + kOffX + s * kBandBytes, 16384u, 1024u, kSwizzle128B);
-#pragma unroll
       for (int p = 0; p < 2; ++p) {
-        // ---- S1: D1 = T_p · X  (8 K-steps of 16 band rows, A strip hi + lo)
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t so = (14u - 2u * k) * 16u;  // strip offset, 16-byte units
-          mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + (2 * p) * (kStripBytes / 16) + so),
-                           bx + 128u * k, id128, k > 0 ? 1u : 0u);
-          mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + (2 * p + 1) * (kStripBytes / 16) + so),
-                           bx + 128u * k, id128, 1u);
-        }
-        mma_commit_elect(s1done);
-        if (p == 0 && lane == 0) stamp(P, it, 8);
-        if (p == 1) mma_commit_elect(&xempty[s]);
         // ---- S3: row forward, A = packed D1 from TMEM
         mbar_wait(c1, ph);
         tc_fence_after();
@@ -320,13 +332,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_f16_ts_elect(d, tmem + kTD1 + 64u + pc, b3, id16, 1u);
             mma_f16_ts_elect(d, tmem + kTD1 + pc, b3 + 32u, id16, 1u);
           }
+          mma_commit_elect(&s3done[q]);  // E2 cores column phase q while S3 runs q + 1
         }
-        mma_commit_elect(s3done);
-        // ---- S5: row inverse (TS tf32, A = cored D2) into D3 (over D1)
-        mbar_wait(e2, ph);
-        tc_fence_after();
+        // ---- S5: row inverse (TS tf32, A = cored D2) into D3 (over D1): column
+        // phase q starts as soon as its coefficients are cored; D3 overwrites
+        // the packed D1, so every S3 MMA must have completed (s3done[1])
+        mbar_wait(&s3done[1], ph);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
+          mbar_wait(&e2[q], ph);
+          tc_fence_after();
 #pragma unroll
           for (int j = 0; j < (q == 0 ? 8 : 7); ++j) {
 #pragma unroll
@@ -336,8 +351,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         mma_commit_elect(s5done);
-        // ---- S7: column inverse, D4 += T_pᵀ · B7 (hi + lo)
+        // E3 has read D3: the next row phase's S1 (this band's p = 1, or the
+        // next band's p = 0) goes first, so its C1 overlaps this phase's S7
+        // (measured neutral: the in-order tensor pipe then runs S7 ahead of
+        // the next S3 — kept for the shorter C1 wait)
         mbar_wait(e3, ph);
+        auto next_s1 = [&]() {
+          if (p == 0) {
+            issue_s1(s, 1);
+          } else if (t + static_cast<int>(gridDim.x) < P.nregions) {
+            const int s2 = (it + 1) & 1;
+            mbar_wait(&xfull[s2], ((it + 1) >> 1) & 1);
+            mbar_wait(&xready[s2], ((it + 1) >> 1) & 1);
+            if (lane == 0) stamp(P, it + 1, 7);
+            issue_s1(s2, 0);
+          }
+        };
+        next_s1();
+        // ---- S7: column inverse, D4 += T_pᵀ · B7 (hi + lo)
         if (p == 0 && it > 0) mbar_wait(e4, (it - 1) & 1);  // previous band's E4 read D4
         tc_fence_after();
 #pragma unroll
@@ -390,22 +421,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(c1);
         if (et == 0) stamp(P, it, 12 * p + 1);
-        // ---- E2: coring of D2 (lane f, columns 16*(8q+j) + l) in place
-        mbar_wait(s3done, ph);
-        tc_fence_after();
-        if (et == 0) stamp(P, it, 12 * p + 2);
-        if (sp == 0) dbg_dump(P, it, 1, p, tl + kTD2, row, 240);
-        {
-          const bool dc_row = (row & 15) == 0;
-          const float thr = P.threshold;
-          uint32_t v[4][16];
+        // ---- E2: coring of D2 (lane f, columns 16*(8q+j) + l) in place, one
+        // column phase at a time (chunks 0-7: q = 0, 8-14: q = 1)
+        const bool dc_row = (row & 15) == 0;
+        const float thr = P.threshold;
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (sp + 4 * c < 15) tmem_ld16(tl + kTD2 + 16u * (sp + 4 * c), v[c]);
+        for (int q = 0; q < 2; ++q) {
+          mbar_wait(&s3done[q], ph);
+          tc_fence_after();
+          if (et == 0) stamp(P, it, 12 * p + (q == 0 ? 2 : 6));
+          if (sp == 0 && q == 1) dbg_dump(P, it, 1, p, tl + kTD2, row, 240);
+          uint32_t v[2][16];
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            if (8 * q + sp + 4 * c < 15) tmem_ld16(tl + kTD2 + 16u * (8 * q + sp + 4 * c), v[c]);
           tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if (sp + 4 * c < 15) {
+          for (int c = 0; c < 2; ++c) {
+            const int ch = 8 * q + sp + 4 * c;
+            if (ch < 15) {
               const uint32_t dc = v[c][0];
 #pragma unroll
               for (int l = 0; l < 16; ++l) {
@@ -418,13 +452,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 v[c][l] = __float_as_uint(y);
               }
               if (dc_row) v[c][0] = dc;  // DC coefficient kept
-              tmem_st16(tl + kTD2 + 16u * (sp + 4 * c), v[c]);
+              tmem_st16(tl + kTD2 + 16u * ch, v[c]);
             }
           }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&e2[q]);
         }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(e2);
         if (et == 0) stamp(P, it, 12 * p + 3);
         // ---- E3: D3 (lane f, 128 columns) -> B7[f][c] hi/lo (MN-major, 128B swizzle)
         mbar_wait(s5done, ph);
@@ -547,18 +581,11 @@ static void build_consts(uint8_t* out) {
     const float f = static_cast<float>(v);
     std::memcpy(dst + (n / 8) * 512 + (kk / 4) * 128 + (n % 8) * 16 + (kk % 4) * 4, &f, 4);
   };
-  // S1 strips: row g, K = band row within the K-step.  Step k reads rows
+  // S1 strip: row g, K = band row within the K-step.  Step k reads rows
   // g = f + 112 - 16k, so tile i = k sits at g in [112, 128).
-  for (int lo = 0; lo < 2; ++lo) {
-    uint8_t* s0 = out + (0 * 2 + lo) * dct::kStripBytes;
-    uint8_t* s1 = out + (1 * 2 + lo) * dct::kStripBytes;
+  for (int lo = 0; lo < 2; ++lo)
     for (int k = 0; k < 16; ++k)
-      for (int kk = 0; kk < 16; ++kk) {
-        put16(s0, 112 + k, kk, D[k][kk], lo);                       // p = 0: tile rows 16i..
-        if (kk < 8) put16(s1, 96 + k, kk, D[k][kk + 8], lo);      // p = 1: tile i-1, 2nd half
-        if (kk >= 8) put16(s1, 112 + k, kk, D[k][kk - 8], lo);    // p = 1: tile i, 1st half
-      }
-  }
+      for (int kk = 0; kk < 16; ++kk) put16(out + lo * dct::kStripBytes, 112 + k, kk, D[k][kk], lo);
   // S7 strip: A7[r][kk] = Dw[kk][r - 16k - 8p] at g = r + 120 - 16k - 8p
   for (int m = 0; m < 16; ++m)
     for (int kk = 0; kk < 16; ++kk) put16(out + dct::kCS7, 120 + m, kk, D[kk][m], 0);
