@@ -51,19 +51,6 @@ void get_trace(unsigned long long** buf, int* ctas, int* tiles);
 
 namespace dct {
 
-constexpr int kEpiThreads = 512;                 // warps 2-17: epilogue
-constexpr int kThreads = 64 + kEpiThreads;    // warp 0 loader, warp 1 MMA
-constexpr int kBand = 128;
-constexpr int kOut = 112;
-constexpr uint32_t kBandBytes = kBand * kBand * 2;  // bf16 band, two 64-col SW128 halves
-
-// smem layout (bytes from the 1024-aligned base)
-constexpr uint32_t kOffX = 0;                            // 2 band buffers
-constexpr uint32_t kOffB7 = kOffX + 2 * kBandBytes;      // S7 B operand: hi, lo (32 KB each)
-constexpr uint32_t kB7Lo = 32768;
-constexpr uint32_t kOffOut = kOffB7 + 2 * 32768;         // 112 x 112 staging (f32 worst case)
-constexpr uint32_t kOutBytes = kOut * kOut * 4;
-constexpr uint32_t kOffC = kOffOut + ((kOutBytes + 1023) / 1024) * 1024;
 // constants (built on the host, one bulk copy per CTA):
 //   S1 strip : hi, lo: 240 rows x 16 K, K-major core matrices (7680 B each)
 //   S7 strip : 248 rows x 16 K
@@ -74,13 +61,37 @@ constexpr uint32_t kCS7 = 2 * kStripBytes;
 constexpr uint32_t kCB3 = kCS7 + 7936;
 constexpr uint32_t kCB5 = kCB3 + 1024;
 constexpr uint32_t kConstBytes = kCB5 + 1024;
-constexpr uint32_t kOffBar = kOffC + kConstBytes;
-constexpr uint32_t kSmem = kOffBar + 256 + 1024;
+constexpr int kBandRows = 128;  // band rows (input), 112 output rows
+constexpr int kOutRows = 112;
 
-// TMEM columns
-constexpr uint32_t kTD1 = 0;    // D1 f32 / packed pairs (hi 0..63, lo 64..127) / D3
-constexpr uint32_t kTD2 = 128;  // 240 columns
-constexpr uint32_t kTD4 = 368;  // 128 columns
+constexpr uint32_t round1k(uint32_t v) { return (v + 1023u) / 1024u * 1024u; }
+
+// Band geometry: BW = 128 input columns (112 out, one CTA per SM, 512 TMEM
+// columns) or 64 (48 out, two CTAs per SM sharing the tensor pipe and the
+// TMEM ports, 256 TMEM columns each).
+template <int BW>
+struct Geo {
+  static constexpr int kOutW = BW - 16;
+  static constexpr int kSplits = BW / 32;  // epilogue warps per TMEM lane quarter
+  static constexpr int kEpiThreads = 128 * kSplits;
+  static constexpr int kThreads = 64 + kEpiThreads;  // + loader warp, MMA warp
+  static constexpr int kNq0 = BW / 16, kNq1 = BW / 16 - 1;  // tiles per column phase
+  static constexpr int kChunks = kNq0 + kNq1;                // 16-column chunks of D2
+  static constexpr uint32_t kBandBytes = kBandRows * BW * 2;  // BW/64 SW128 boxes
+  static constexpr uint32_t kOffX = 0;                        // 2 band buffers
+  static constexpr uint32_t kB7Lo = kBandRows * BW * 2;       // S7 B operand hi, lo
+  static constexpr uint32_t kOffB7 = 2 * kBandBytes;
+  static constexpr uint32_t kOffOut = kOffB7 + 2 * kB7Lo;     // staging (f32 worst case)
+  static constexpr uint32_t kOffC = kOffOut + round1k(kOutRows * kOutW * 4);
+  static constexpr uint32_t kOffBar = kOffC + kConstBytes;
+  static constexpr uint32_t kSmem = kOffBar + 256 + 1024;
+  // TMEM columns: D1 f32 / packed pairs (hi [0, BW/2), lo [BW/2, BW)) / D3;
+  // D2 (kChunks x 16); D4 (BW)
+  static constexpr uint32_t kTD1 = 0, kTD2 = BW, kTD4 = BW + 16 * kChunks;
+  static constexpr int kTmemCols = BW == 128 ? 512 : 256;
+  static constexpr int kMinBlocks = BW == 128 ? 1 : 2;
+  static_assert(kTD4 + BW <= static_cast<uint32_t>(kTmemCols), "TMEM budget");
+};
 
 struct Params {
   int planes, H, W, nry, nrx, nregions;
@@ -159,14 +170,16 @@ __device__ __forceinline__ uint32_t hi_lo(float a, float b, uint32_t* lo) {
 
 // Clamp-to-edge for border bands: replicate the edge row / column of the
 // image into the (TMA zero-filled) 8 samples beyond it.  Whole warp.
+template <int BW>
 __device__ __forceinline__ void fix_edges(uint8_t* bx, int Y, int X, int H, int W, int lane) {
+  constexpr int kChunkCols = BW / 8;  // 16-byte chunks per band row
   int r0[2], rs[2], nr = 0;
   if (Y == 0) { r0[nr] = 0; rs[nr] = 8; ++nr; }
-  if (H - Y + 8 < kBand) { r0[nr] = H - Y + 8; rs[nr] = H - Y + 7; ++nr; }
+  if (H - Y + 8 < kBandRows) { r0[nr] = H - Y + 8; rs[nr] = H - Y + 7; ++nr; }
   for (int e = 0; e < nr; ++e) {
-    const int rows = min(8, kBand - r0[e]);
-    for (int idx = lane; idx < rows * 16; idx += 32) {
-      const int br = r0[e] + idx / 16, j = idx % 16, h = j >> 3, cc = j & 7;
+    const int rows = min(8, kBandRows - r0[e]);
+    for (int idx = lane; idx < rows * kChunkCols; idx += 32) {
+      const int br = r0[e] + idx / kChunkCols, j = idx % kChunkCols, h = j >> 3, cc = j & 7;
       const uint4 v = *reinterpret_cast<const uint4*>(bx + h * 16384 + rs[e] * 128 +
                                                       ((cc ^ (rs[e] & 7)) << 4));
       *reinterpret_cast<uint4*>(bx + h * 16384 + br * 128 + ((cc ^ (br & 7)) << 4)) = v;
@@ -175,9 +188,9 @@ __device__ __forceinline__ void fix_edges(uint8_t* bx, int Y, int X, int H, int 
   __syncwarp();
   int c0[2], cs[2], nc = 0;
   if (X == 0) { c0[nc] = 0; cs[nc] = 8; ++nc; }
-  if (W - X + 8 < kBand) { c0[nc] = W - X + 8; cs[nc] = W - X + 7; ++nc; }
+  if (W - X + 8 < BW) { c0[nc] = W - X + 8; cs[nc] = W - X + 7; ++nc; }
   for (int e = 0; e < nc; ++e) {
-    for (int br = lane; br < kBand; br += 32) {
+    for (int br = lane; br < kBandRows; br += 32) {
       const uint32_t v = *reinterpret_cast<const uint16_t*>(bx + sw_off(br, cs[e]));
       const uint32_t w = v | (v << 16);
       *reinterpret_cast<uint4*>(bx + sw_off(br, c0[e])) = make_uint4(w, w, w, w);
@@ -200,15 +213,21 @@ __device__ __forceinline__ Region region_of(const Params& P, int t) {
   return r;
 }
 
-template <typename OutT, bool SOFT>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BW, typename OutT, bool SOFT>
+__global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     dct16_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                  const __grid_constant__ Params P) {
+  using G = Geo<BW>;
+  constexpr int kEpiThreads = G::kEpiThreads;
+  constexpr uint32_t kBandBytes = G::kBandBytes, kOffX = G::kOffX, kOffB7 = G::kOffB7;
+  constexpr uint32_t kB7Lo = G::kB7Lo, kOffOut = G::kOffOut, kOffC = G::kOffC;
+  constexpr uint32_t kTD1 = G::kTD1, kTD2 = G::kTD2, kTD4 = G::kTD4;
+  constexpr int kOut = G::kOutW;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_s = smem_u32(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_s - raw_s);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kOffBar);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + G::kOffBar);
   uint64_t* xfull = bars;        // [2]
   uint64_t* xempty = bars + 2;   // [2]
   uint64_t* xready = bars + 4;   // [2]
@@ -245,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tm_in);
     prefetch_tmap(&tm_out);
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) tmem_alloc<G::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -261,25 +280,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
       const int s = it & 1;
       const Region R = region_of(P, t);
-      const int Y = R.ry * kOut, X = R.rx * kOut;
+      const int Y = R.ry * kOutRows, X = R.rx * kOut;
       uint8_t* dst = base + kOffX + s * kBandBytes;
       if (lane == 0) {
         mbar_wait(&xempty[s], ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&xfull[s], kBandBytes);
-        tma_load_3d(dst, &tm_in, &xfull[s], X - 8, Y - 8, R.p);
-        tma_load_3d(dst + kBand * 128, &tm_in, &xfull[s], X - 8 + 64, Y - 8, R.p);
+#pragma unroll
+        for (int h = 0; h < BW / 64; ++h)
+          tma_load_3d(dst + h * kBandRows * 128, &tm_in, &xfull[s], X - 8 + 64 * h, Y - 8, R.p);
       }
       __syncwarp();
-      const bool edge = Y == 0 || X == 0 || P.H - Y + 8 < kBand || P.W - X + 8 < kBand;
+      const bool edge = Y == 0 || X == 0 || P.H - Y + 8 < kBandRows || P.W - X + 8 < BW;
       if (edge) {
         mbar_wait(&xfull[s], (it >> 1) & 1);
-        fix_edges(dst, Y, X, P.H, P.W, lane);
+        fix_edges<BW>(dst, Y, X, P.H, P.W, lane);
       }
       if (lane == 0) mbar_arrive(&xready[s]);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t id128 = make_idesc(kFmtBF16, 128, 128, /*A K-major*/ 0, /*B MN*/ 1);
+    const uint32_t id128 = make_idesc(kFmtBF16, 128, BW, /*A K-major*/ 0, /*B MN*/ 1);
     const uint32_t id16 = make_idesc(kFmtBF16, 128, 16, 0, 0);
     const uint32_t idtf = make_idesc(kFmtTF32, 128, 16, 0, 0);
     const uint64_t a_tmpl = make_sdesc(0u, 128u, 256u, kSwizzleNone);
@@ -325,11 +345,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
 #pragma unroll
-          for (int j = 0; j < (q == 0 ? 8 : 7); ++j) {
+          for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j) {
             const uint32_t pc = 8u * j + 4u * q;  // packed column of the tile's first sample
-            const uint32_t d = tmem + kTD2 + 16u * (8 * q + j);
+            const uint32_t d = tmem + kTD2 + 16u * (G::kNq0 * q + j);
             mma_f16_ts_elect(d, tmem + kTD1 + pc, b3, id16, 0u);
-            mma_f16_ts_elect(d, tmem + kTD1 + 64u + pc, b3, id16, 1u);
+            mma_f16_ts_elect(d, tmem + kTD1 + BW / 2 + pc, b3, id16, 1u);
             mma_f16_ts_elect(d, tmem + kTD1 + pc, b3 + 32u, id16, 1u);
           }
           mma_commit_elect(&s3done[q]);  // E2 cores column phase q while S3 runs q + 1
@@ -343,10 +363,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&e2[q], ph);
           tc_fence_after();
 #pragma unroll
-          for (int j = 0; j < (q == 0 ? 8 : 7); ++j) {
+          for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j) {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              mma_tf32_ts_elect(tmem + kTD1 + 16u * j + 8u * q, tmem + kTD2 + 16u * (8 * q + j) + 8u * h,
+              mma_tf32_ts_elect(tmem + kTD1 + 16u * j + 8u * q,
+                                tmem + kTD2 + 16u * (G::kNq0 * q + j) + 8u * h,
                                 b5 + 16u * h, idtf, (q > 0 || h > 0) ? 1u : 0u);
           }
         }
@@ -382,10 +403,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2-17)
-    // 16 warps: warp w serves TMEM lane quarter w % 4 (hardware rule) and
-    // column split sp = (w - 2) / 4, so each step's ALU work is spread over
-    // four warps per scheduler.
+    // ------------------------------------------------------------ epilogue (warps 2..)
+    // 4 x kSplits warps: warp w serves TMEM lane quarter w % 4 (hardware
+    // rule) and the 32-column split sp = (w - 2) / 4, so each step's ALU work
+    // is spread over kSplits warps per scheduler.
     const int quarter = warp & 3;
     const int sp = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;  // TMEM lane
@@ -396,13 +417,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
       const Region R = region_of(P, t);
-      const int Y = R.ry * kOut, X = R.rx * kOut;
+      const int Y = R.ry * kOutRows, X = R.rx * kOut;
       for (int p = 0; p < 2; ++p) {
-        // ---- C1: D1 (f32, lane f, 128 columns) -> bf16 pairs: hi at 0..63, lo at 64..127
+        // ---- C1: D1 (f32, lane f, BW columns) -> bf16 pairs: hi at [0, BW/2), lo at [BW/2, BW)
         mbar_wait(s1done, ph);
         tc_fence_after();
         if (et == 0) stamp(P, it, 12 * p + 0);
-        if (sp == 0) dbg_dump(P, it, 0, p, tl + kTD1, row, 128);
+        if (sp == 0) dbg_dump(P, it, 0, p, tl + kTD1, row, BW);
         {
           uint32_t v[2][16];
           tmem_ld16(tl + kTD1 + 32u * sp, v[0]);
@@ -415,14 +436,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             hi[e] = hi_lo(__uint_as_float(v[e >> 3][(2 * e) & 15]),
                           __uint_as_float(v[e >> 3][((2 * e) & 15) + 1]), &lo[e]);
           tmem_st16(tl + kTD1 + 16u * sp, hi);
-          tmem_st16(tl + kTD1 + 64u + 16u * sp, lo);
+          tmem_st16(tl + kTD1 + BW / 2 + 16u * sp, lo);
         }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(c1);
         if (et == 0) stamp(P, it, 12 * p + 1);
-        // ---- E2: coring of D2 (lane f, columns 16*(8q+j) + l) in place, one
-        // column phase at a time (chunks 0-7: q = 0, 8-14: q = 1)
+        // ---- E2: coring of D2 (lane f, columns 16*(kNq0*q+j) + l) in place,
+        // one column phase at a time
         const bool dc_row = (row & 15) == 0;
         const float thr = P.threshold;
 #pragma unroll
@@ -430,16 +451,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&s3done[q], ph);
           tc_fence_after();
           if (et == 0) stamp(P, it, 12 * p + (q == 0 ? 2 : 6));
-          if (sp == 0 && q == 1) dbg_dump(P, it, 1, p, tl + kTD2, row, 240);
+          if (sp == 0 && q == 1) dbg_dump(P, it, 1, p, tl + kTD2, row, 16 * G::kChunks);
+          const int ch0 = q == 0 ? 0 : G::kNq0, ch1 = q == 0 ? G::kNq0 : G::kChunks;
           uint32_t v[2][16];
 #pragma unroll
           for (int c = 0; c < 2; ++c)
-            if (8 * q + sp + 4 * c < 15) tmem_ld16(tl + kTD2 + 16u * (8 * q + sp + 4 * c), v[c]);
+            if (ch0 + sp + G::kSplits * c < ch1)
+              tmem_ld16(tl + kTD2 + 16u * (ch0 + sp + G::kSplits * c), v[c]);
           tmem_wait_ld();
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const int ch = 8 * q + sp + 4 * c;
-            if (ch < 15) {
+            const int ch = ch0 + sp + G::kSplits * c;
+            if (ch < ch1) {
               const uint32_t dc = v[c][0];
 #pragma unroll
               for (int l = 0; l < 16; ++l) {
@@ -460,11 +483,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(&e2[q]);
         }
         if (et == 0) stamp(P, it, 12 * p + 3);
-        // ---- E3: D3 (lane f, 128 columns) -> B7[f][c] hi/lo (MN-major, 128B swizzle)
+        // ---- E3: D3 (lane f, BW columns) -> B7[f][c] hi/lo (MN-major, 128B swizzle)
         mbar_wait(s5done, ph);
         tc_fence_after();
         if (et == 0) stamp(P, it, 12 * p + 4);
-        if (sp == 0) dbg_dump(P, it, 2, p, tl + kTD1, row, 128);
+        if (sp == 0) dbg_dump(P, it, 2, p, tl + kTD1, row, BW);
         {
           uint8_t* b7 = base + kOffB7;
           uint32_t v[2][16];
@@ -493,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(s7done, ph ^ 1);
       tc_fence_after();
       if (et == 0) stamp(P, it, 22);
-      if (sp == 0) dbg_dump(P, it, 3, 0, tl + kTD4, row, 128);
+      if (sp == 0) dbg_dump(P, it, 3, 0, tl + kTD4, row, BW);
       if (et == 0) bulk_wait_read0();
       named_bar_sync(1, kEpiThreads);
       {
@@ -503,9 +526,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(e4);
-        if (row >= 8 && row < 8 + kOut) {
+        if (row >= 8 && row < 8 + kOutRows) {
           uint8_t* orow = base + kOffOut + (row - 8) * kOut * sizeof(OutT);
-          // band columns 8..119 -> output columns 0..111, 8 at a time
+          // band columns 8..BW-9 -> output columns 0..kOut-1, 8 at a time
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             const int c = 32 * sp + 8 * g;
@@ -541,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<G::kTmemCols>(tmem);
   }
 }
 
@@ -600,13 +623,57 @@ static void build_consts(uint8_t* out) {
     for (int l = 0; l < 16; ++l) put32(out + dct::kCB5, c, l, D[l][c]);
 }
 
-template <typename OutT, bool SOFT>
-static cudaError_t launch_dct(int grid, const CUtensorMap& tin, const CUtensorMap& tout,
+template <int BW, typename OutT, bool SOFT>
+static cudaError_t launch_dct(const CUtensorMap& tin, const CUtensorMap& tout,
                               const dct::Params& P, cudaStream_t stream) {
-  auto k = dct::dct16_kernel<OutT, SOFT>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dct::kSmem);
-  if (e == cudaSuccess) k<<<grid, dct::kThreads, dct::kSmem, stream>>>(tin, tout, P);
-  return e;
+  using G = dct::Geo<BW>;
+  auto k = dct::dct16_kernel<BW, OutT, SOFT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem);
+  if (e != cudaSuccess) return e;
+  const int slots = G::kMinBlocks * sm_count_current();
+  const int grid = P.nregions < slots ? P.nregions : slots;
+  k<<<grid, G::kThreads, G::kSmem, stream>>>(tin, tout, P);
+  return cudaSuccess;
+}
+
+template <int BW>
+static ts_status dct16_run_bw(const void* in, int64_t in_rs, int64_t in_ps, void* out,
+                              int64_t out_rs, int64_t out_ps, int out_dtype, int planes, int H,
+                              int W, float threshold, int soft, const uint8_t* consts,
+                              cudaStream_t stream) {
+  using G = dct::Geo<BW>;
+  const int oes = out_dtype == TS_BF16 ? 2 : 4;
+  dct::Params P;
+  P.planes = planes;
+  P.H = H;
+  P.W = W;
+  P.nry = (H + dct::kOutRows - 1) / dct::kOutRows;
+  P.nrx = (W + G::kOutW - 1) / G::kOutW;
+  P.nregions = planes * P.nry * P.nrx;
+  P.threshold = threshold;
+  P.soft = soft;
+  P.consts = consts;
+  P.dbg = g_dct_dbg;
+  get_trace(&P.trace, &P.trace_ctas, &P.trace_tiles);
+  CUtensorMap tin, tout;
+  ts_status st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs,
+                                in_ps, 64, dct::kBandRows, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != TS_OK) return st;
+  st = encode_tmap_3d(&tout,
+                      out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                      oes, out, W, H, planes, out_rs, out_ps, G::kOutW, dct::kOutRows,
+                      CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st != TS_OK) return st;
+  cudaError_t e;
+  if (out_dtype == TS_BF16)
+    e = soft ? launch_dct<BW, __nv_bfloat16, true>(tin, tout, P, stream)
+             : launch_dct<BW, __nv_bfloat16, false>(tin, tout, P, stream);
+  else
+    e = soft ? launch_dct<BW, float, true>(tin, tout, P, stream)
+             : launch_dct<BW, float, false>(tin, tout, P, stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "dct16 launch");
 }
 
 ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, void* out,
@@ -634,39 +701,14 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
     e = cudaMemcpy(d_consts[dev], h, dct::kConstBytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_error(e, "dct16 consts copy");
   }
-  dct::Params P;
-  P.planes = planes;
-  P.H = H;
-  P.W = W;
-  P.nry = (H + dct::kOut - 1) / dct::kOut;
-  P.nrx = (W + dct::kOut - 1) / dct::kOut;
-  P.nregions = planes * P.nry * P.nrx;
-  P.threshold = threshold;
-  P.soft = soft;
-  P.consts = d_consts[dev];
-  P.dbg = g_dct_dbg;
-  get_trace(&P.trace, &P.trace_ctas, &P.trace_tiles);
-  CUtensorMap tin, tout;
-  ts_status st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs,
-                                in_ps, 64, dct::kBand, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (st != TS_OK) return st;
-  st = encode_tmap_3d(&tout,
-                      out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                      oes, out, W, H, planes, out_rs, out_ps, dct::kOut, dct::kOut,
-                      CU_TENSOR_MAP_SWIZZLE_NONE);
-  if (st != TS_OK) return st;
-  const int sms = sm_count_current();
-  const int grid = P.nregions < sms ? P.nregions : sms;
-  cudaError_t e;
-  if (out_dtype == TS_BF16)
-    e = soft ? launch_dct<__nv_bfloat16, true>(grid, tin, tout, P, stream)
-             : launch_dct<__nv_bfloat16, false>(grid, tin, tout, P, stream);
-  else
-    e = soft ? launch_dct<float, true>(grid, tin, tout, P, stream)
-             : launch_dct<float, false>(grid, tin, tout, P, stream);
-  if (e == cudaSuccess) e = cudaGetLastError();
-  return e == cudaSuccess ? TS_OK : cuda_error(e, "dct16 launch");
+  // band width: 64 columns (two CTAs per SM overlap one band's MMAs with the
+  // other's TMEM epilogues) unless TSB_DCT_BAND=128
+  const char* v = std::getenv("TSB_DCT_BAND");
+  if (v && std::atoi(v) == 128)
+    return dct16_run_bw<128>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
+                             threshold, soft, d_consts[dev], stream);
+  return dct16_run_bw<64>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
+                          threshold, soft, d_consts[dev], stream);
 }
 
 }  // namespace tsb

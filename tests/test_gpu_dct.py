@@ -66,3 +66,14 @@ def test_denoising_reduces_error():
     clean = (0.5 + 0.4 * np.sin(xx / 17.0) * np.cos(yy / 23.0)).astype(np.float32)
     y = _gpu(x, threshold=0.15)
     assert np.sqrt(((y[0] - clean) ** 2).mean()) < 0.5 * np.sqrt(((x[0] - clean) ** 2).mean())
+
+
+@pytest.mark.parametrize("shape", [(1, 136, 248), (2, 232, 360)])
+def test_full_band_variant_matches_oracle(shape, monkeypatch):
+    """The 128-column band kernel (TSB_DCT_BAND=128; default is 64-column
+    bands, two CTAs per SM) against the oracle."""
+    monkeypatch.setenv("TSB_DCT_BAND", "128")
+    x = _noisy(shape, 5)
+    y = _gpu(x, threshold=0.15, mode="soft")
+    ref = pipelines_ref.dct_denoise(x, 0.15, "soft")
+    assert np.abs(y - ref).max() <= 1e-2
