@@ -259,6 +259,10 @@ TS_API ts_status ts_probe_issue_ts(int variant, long long* cycles, void* stream)
  * chunks of rows x (64 * nbox) through an nr-slot ring (load path only). */
 TS_API ts_status ts_probe_tma(const void* src, int planes, int H, int W, int rows, int nbox, int nr,
                               int grid, void* stream);
+/* TMEM load throughput probe: `warps` warps (multiple of 4) read `cols`
+ * columns of their lane quarter `reps` times with tcgen05.ld.32x32b.x{x}. */
+TS_API ts_status ts_probe_tmem_ld(int x, int warps, int cols, int reps, long long* cycles,
+                                  void* stream);
 TS_API ts_status ts_probe_issue2(int amode, int bmode, int n, int count, int nacc,
                                  long long* cycles, void* stream);
 

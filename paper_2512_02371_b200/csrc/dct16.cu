@@ -162,10 +162,15 @@ __device__ __forceinline__ uint32_t sw_off(int row, int col) {
   return (col >> 6) * 16384u + row * 128u + ((((col & 63) >> 3) ^ (row & 7)) << 4) + (col & 7) * 2u;
 }
 
+// bf16 hi/lo split of a pair with ONE conversion: hi rounds to nearest
+// (F2FP); the residuals a - hi are exact in f32 and are truncated to bf16 by
+// a byte permute (|lo| < 2^-8 |a|, so truncation costs < 2^-16 |a|).  The
+// conversion pipe, not TMEM, bounds the DCT epilogues.
 __device__ __forceinline__ uint32_t hi_lo(float a, float b, uint32_t* lo) {
-  const __nv_bfloat16 ah = __float2bfloat16_rn(a), bh = __float2bfloat16_rn(b);
-  *lo = pack_bf16x2(a - __bfloat162float(ah), b - __bfloat162float(bh));
-  return pack_bf16x2(a, b);
+  const uint32_t h = pack_bf16x2(a, b);  // a -> low half, b -> high half (RNE)
+  const float la = a - __uint_as_float(h << 16), lb = b - __uint_as_float(h & 0xFFFF0000u);
+  *lo = __byte_perm(__float_as_uint(la), __float_as_uint(lb), 0x7632);
+  return h;
 }
 
 // Clamp-to-edge for border bands: replicate the edge row / column of the
@@ -198,6 +203,14 @@ __device__ __forceinline__ void fix_edges(uint8_t* bx, int Y, int X, int H, int 
   }
   fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05 operand reads
   __syncwarp();
+}
+
+// One mbarrier arrival per warp: the lanes' prior TMEM/smem writes and
+// fences are ordered before it by __syncwarp (hundreds of per-thread
+// arrivals on one barrier serialise on the shared-memory atomic unit).
+__device__ __forceinline__ void warp_arrive(uint64_t* bar, int lane) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(bar);
 }
 
 struct Region {
@@ -254,11 +267,11 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     mbar_init(&s3done[1], 1);
     mbar_init(s5done, 1);
     mbar_init(s7done, 1);
-    mbar_init(c1, kEpiThreads);
-    mbar_init(&e2[0], kEpiThreads);
-    mbar_init(&e2[1], kEpiThreads);
-    mbar_init(e3, kEpiThreads);
-    mbar_init(e4, kEpiThreads);
+    mbar_init(c1, kEpiThreads / 32);  // one arrival per epilogue warp
+    mbar_init(&e2[0], kEpiThreads / 32);  // one arrival per epilogue warp
+    mbar_init(&e2[1], kEpiThreads / 32);  // one arrival per epilogue warp
+    mbar_init(e3, kEpiThreads / 32);  // one arrival per epilogue warp
+    mbar_init(e4, kEpiThreads / 32);  // one arrival per epilogue warp
     mbar_init(cbar, 1);
     fence_barrier_init();
     prefetch_tmap(&tm_in);
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(c1);
+        warp_arrive(c1, lane);
         if (et == 0) stamp(P, it, 12 * p + 1);
         // ---- E2: coring of D2 (lane f, columns 16*(kNq0*q+j) + l) in place,
         // one column phase at a time
@@ -480,7 +493,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
           }
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&e2[q]);
+          warp_arrive(&e2[q], lane);
         }
         if (et == 0) stamp(P, it, 12 * p + 3);
         // ---- E3: D3 (lane f, BW columns) -> B7[f][c] hi/lo (MN-major, 128B swizzle)
@@ -508,7 +521,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         }
         tc_fence_before();
         fence_proxy_async_smem();
-        mbar_arrive(e3);
+        warp_arrive(e3, lane);
         if (et == 0) stamp(P, it, 12 * p + 5);
         ph ^= 1;
       }
@@ -525,7 +538,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         tmem_ld16(tl + kTD4 + 32u * sp + 16u, v[1]);
         tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive(e4);
+        warp_arrive(e4, lane);
         if (row >= 8 && row < 8 + kOutRows) {
           uint8_t* orow = base + kOffOut + (row - 8) * kOut * sizeof(OutT);
           // band columns 8..BW-9 -> output columns 0..kOut-1, 8 at a time

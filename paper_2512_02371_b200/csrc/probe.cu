@@ -549,3 +549,89 @@ extern "C" ts_status ts_probe_tma(const void* src, int planes, int H, int W, int
   }
   return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_tma launch");
 }
+
+// TMEM load throughput probe: `warps` warps (4 per lane quarter group) each
+// read `cols` columns of their lane quarter with tcgen05.ld.32x32b.x{16,32,64}
+// `reps` times; reports cycles for the whole CTA.
+namespace tsb {
+template <int X>
+__device__ __forceinline__ void tmem_ldx(uint32_t taddr, uint32_t* r);
+template <>
+__device__ __forceinline__ void tmem_ldx<16>(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+template <>
+__device__ __forceinline__ void tmem_ldx<32>(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+template <int X>
+__global__ void __launch_bounds__(512, 1) probe_tmem_ld_kernel(int cols, int reps, long long* cycles,
+                                                               unsigned* sink) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const int nw = blockDim.x / 32;
+  const int per_quarter = nw / 4;        // warps sharing a lane quarter
+  const int sub = (warp >> 2);           // which of them
+  const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  const int my_cols = cols / per_quarter;
+  uint32_t acc = 0;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    for (int c = 0; c < my_cols; c += X) {
+      uint32_t v[X];
+      tmem_ldx<X>(tmem + lane_off + static_cast<uint32_t>(sub * my_cols + c), v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < X; ++i) acc ^= v[i];
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) *cycles = t1 - t0;
+  if (acc == 0x12345678u) *sink = acc;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+}  // namespace tsb
+
+extern "C" ts_status ts_probe_tmem_ld(int x, int warps, int cols, int reps, long long* cycles,
+                                      void* stream) {
+  using namespace tsb;
+  if ((x != 16 && x != 32) || warps < 4 || warps > 16 || warps % 4 || cols < 16 || cols > 512 ||
+      reps < 1 || !cycles)
+    return set_error(TS_ERR_INVALID, "probe_tmem_ld: bad arguments");
+  static unsigned* sink = nullptr;
+  if (!sink && cudaMalloc(&sink, 4) != cudaSuccess) return set_error(TS_ERR_CUDA, "probe sink");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (x == 16)
+    probe_tmem_ld_kernel<16><<<1, warps * 32, 0, s>>>(cols, reps, cycles, sink);
+  else
+    probe_tmem_ld_kernel<32><<<1, warps * 32, 0, s>>>(cols, reps, cycles, sink);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_tmem_ld launch");
+}
