@@ -35,8 +35,15 @@ ts_status encode_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, cons
 namespace apass {
 
 constexpr int kThreads = 128;
-constexpr int kRing = 6;
-constexpr uint32_t kStep = 4096;  // one K-step of A: 128 x 16 bf16
+// ring slot: vertical = one K-step (16 rows x 128 columns, two 64-column
+// boxes); horizontal = four K-steps (128 rows x 64 columns, one 128B-swizzled
+// K-major box: 128-byte rows keep the TMA efficient)
+template <bool VERT>
+struct Ring {
+  static constexpr int kSlots = VERT ? 6 : 4;
+  static constexpr uint32_t kSlot = VERT ? 4096u : 16384u;
+  static constexpr int kSteps = VERT ? 1 : 4;  // K-steps per slot
+};
 
 struct Params {
   AxisDev ax;
@@ -55,7 +62,9 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_s - raw_s);
   const uint32_t tile_bytes = static_cast<uint32_t>(P.ax.tile_bytes);
-  // [ring kRing x 4 KB][B tiles of the group][staging][barriers]
+  // [ring][B tiles of the group][staging][barriers]
+  using RG = Ring<VERT>;
+  constexpr int kRing = RG::kSlots;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + P.off_bar);
   uint64_t* full = bars;
   uint64_t* empty = bars + kRing;
@@ -97,18 +106,18 @@ __global__ void __launch_bounds__(kThreads)
       }
       int s = 0;
       uint32_t ph = 0;
+      const int nslot = (nq + RG::kSteps - 1) / RG::kSteps;
       for (int j = 0; j < nblk; ++j) {
         const int ws = __ldg(P.ax.tab + b0 + j) >> 16;  // window start (signed)
-        for (int q = 0; q < nq; ++q) {
+        for (int q = 0; q < nslot; ++q) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], kStep);
-          uint8_t* dst = base + s * kStep;
+          mbar_arrive_expect_tx(&full[s], RG::kSlot);
+          uint8_t* dst = base + s * RG::kSlot;
           if (VERT) {  // rows ws+16q.., columns 128*strip.. as two 64-column boxes
             tma_load_3d(dst, &tm_in, &full[s], 128 * strip, ws + 16 * q, p);
             tma_load_3d(dst + 2048, &tm_in, &full[s], 128 * strip + 64, ws + 16 * q, p);
-          } else {     // rows 128*strip.., columns ws+16q.. as two 8-column boxes
-            tma_load_3d(dst, &tm_in, &full[s], ws + 16 * q, 128 * strip, p);
-            tma_load_3d(dst + 2048, &tm_in, &full[s], ws + 16 * q + 8, 128 * strip, p);
+          } else {     // rows 128*strip.., columns ws+64q.. as one 64-column box
+            tma_load_3d(dst, &tm_in, &full[s], ws + 64 * q, 128 * strip, p);
           }
           if (++s == kRing) {
             s = 0;
@@ -121,19 +130,28 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, VERT ? 1u : 0u, 0u);
     const uint64_t bd0 = make_sdesc(base_s + P.off_b, 128u, static_cast<uint32_t>(P.ax.K) * 16u,
                                     kSwizzleNone);
+    // vertical: MN-major SW128 (64-column atoms 2 KB apart, 8-row groups at
+    // 1 KB); horizontal: K-major SW128 (8-row groups at 1 KB, K-steps are
+    // 32-byte advances inside the swizzle atom)
     const uint64_t ad0 = VERT ? make_sdesc(base_s, 2048u, 1024u, kSwizzle128B)
-                              : make_sdesc(base_s, 2048u, 128u, kSwizzleNone);
+                              : make_sdesc(base_s, 16u, 1024u, kSwizzle128B);
     mbar_wait(wbar, 0);
     int s = 0;
     uint32_t ph = 0;
     for (int j = 0; j < nblk; ++j) {
       const uint64_t bdj = bd0 + static_cast<uint64_t>(j * (tile_bytes >> 4));
-      for (int q = 0; q < nq; ++q) {
+      for (int q0 = 0; q0 < nq; q0 += RG::kSteps) {
         mbar_wait(&full[s], ph);
         __syncwarp();
         tc_fence_after();
-        mma_f16_ss_elect(tmem + 16u * j, ad0 + static_cast<uint64_t>(s * (kStep >> 4)),
-                         bdj + 16u * q, idesc, q > 0 ? 1u : 0u);
+        const uint64_t ads = ad0 + static_cast<uint64_t>(s * (RG::kSlot >> 4));
+#pragma unroll
+        for (int u = 0; u < RG::kSteps; ++u) {
+          const int q = q0 + u;
+          if (q < nq)
+            mma_f16_ss_elect(tmem + 16u * j, ads + static_cast<uint64_t>(u * 2), bdj + 16u * q,
+                             idesc, q > 0 ? 1u : 0u);
+        }
         mma_commit_elect(&empty[s]);
         if (++s == kRing) {
           s = 0;
@@ -243,7 +261,9 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   const uint32_t tb = static_cast<uint32_t>(a->tile_bytes);
   const int64_t base_units = static_cast<int64_t>(planes) * a->nb * P.nstrip;
   P.nbg = 1;
-  while (P.nbg < 8 && base_units / (2 * P.nbg) >= 148 * 64 && (2u * P.nbg) * tb <= 32768u)
+  // (thresholds measured on B200: 4K->540p and 2048^2->{143,450,921}^2)
+  const int64_t want = dim == 0 ? 148 * 64 : 148 * 24;
+  while (P.nbg < 8 && base_units / (2 * P.nbg) >= want && (2u * P.nbg) * tb <= 32768u)
     P.nbg *= 2;
   if (const char* f = std::getenv("TSB_APASS_NBG")) P.nbg = std::atoi(f) > 0 ? std::atoi(f) : 1;
   if (P.nbg > P.nb) P.nbg = P.nb;
@@ -251,7 +271,8 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   const int64_t units = static_cast<int64_t>(planes) * P.ngroups * P.nstrip;
   if (units > 0x7FFFFFFF) return set_error(TS_ERR_UNSUPPORTED, "axis_pass: too many blocks");
   P.nunits = static_cast<int>(units);
-  P.off_b = apass::kRing * apass::kStep;
+  P.off_b = dim == 0 ? apass::Ring<true>::kSlots * apass::Ring<true>::kSlot
+                     : apass::Ring<false>::kSlots * apass::Ring<false>::kSlot;
   P.off_out = P.off_b + ((static_cast<uint32_t>(P.nbg) * tb + 1023u) & ~1023u);
   P.off_bar = P.off_out + ((128u * 16u * P.nbg * oes + 1023u) & ~1023u);
   const uint32_t smem = P.off_bar + 256u + 1024u;
@@ -262,7 +283,7 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
                         64, 16, CU_TENSOR_MAP_SWIZZLE_128B);
   else
     st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs, in_ps,
-                        8, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+                        64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TS_OK) return st;
   const CUtensorMapDataType odt =
       out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
