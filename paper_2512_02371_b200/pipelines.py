@@ -213,3 +213,39 @@ def denoise_dct16(x, threshold: float = 0.15, mode: str = "hard", *, out_dtype=N
 def separable(x, rows: "_axis.Axis", cols: "_axis.Axis", *, out_dtype=None):
     """Apply explicit axes: out = rows · x · colsᵀ per plane."""
     return _run(x, rows, cols, out_dtype)
+
+
+_LANES = {}
+
+
+def run_from_host(fn, host_in, host_out, *, chunk_planes: int = 12, lanes: int = 3):
+    """Stream a batch of planes from (pinned) host memory through `fn` (any
+    pipeline of this module) and back: chunks of `chunk_planes` planes rotate
+    over `lanes` CUDA streams, so the host->device copy of one chunk, the
+    kernels of another and the device->host copy of a third overlap (PCIe is
+    full duplex).  Enqueued on the current device; the current stream waits
+    for all of it, so synchronising that stream (or the device) completes the
+    batch.  host_out must be preallocated with fn's output shape."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cur = torch.cuda.current_stream(dev)
+    key = (dev.index, lanes)
+    streams = _LANES.get(key)
+    if streams is None:
+        streams = _LANES[key] = [torch.cuda.Stream(dev) for _ in range(lanes)]
+    start = torch.cuda.Event()
+    start.record(cur)
+    P = host_in.shape[0]
+    for i, c0 in enumerate(range(0, P, chunk_planes)):
+        n = min(chunk_planes, P - c0)
+        s = streams[i % lanes]
+        s.wait_event(start)
+        with torch.cuda.stream(s):
+            xd = host_in[c0:c0 + n].to(dev, non_blocking=True)
+            y = fn(xd)
+            host_out[c0:c0 + n].copy_(y, non_blocking=True)
+            xd.record_stream(s)
+            y.record_stream(s)
+    for s in streams:
+        cur.wait_stream(s)
+    return host_out

@@ -81,3 +81,14 @@ def test_f32_output_odd_width():
     y = _gpu(pipelines.resample, x, out_h=25, out_w=39)
     ref = pipelines_ref.resample(x, 25, 39)
     assert np.abs(y - ref).max() <= TOL
+
+
+def test_run_from_host_matches_device_path():
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = torch.rand((30, 96, 160)).bfloat16().pin_memory()
+    out = torch.empty((30, 48, 80), dtype=torch.bfloat16).pin_memory()
+    pipelines.run_from_host(pipelines.downsample2x, x, out, chunk_planes=4, lanes=3)
+    torch.cuda.synchronize()
+    ref = pipelines.downsample2x(x.cuda()).cpu()
+    assert torch.equal(out, ref)
