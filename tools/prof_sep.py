@@ -1,4 +1,7 @@
 """Profiling driver: a few launches of the 4K->1080p Lanczos kernel (8 frames)."""
+import os as _os, sys as _sys
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
+
 import sys
 import torch
 from paper_2512_02371_b200 import pipelines

@@ -1,3 +1,5 @@
+import os as _os, sys as _sys
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import json, sys, torch, numpy as np
 from paper_2512_02371_b200 import pipelines, _lib
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 8
