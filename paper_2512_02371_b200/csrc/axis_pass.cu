@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kThreads)
     if (lane == 0) {
       mbar_arrive_expect_tx(wbar, tile_bytes * nblk);
       for (int j = 0; j < nblk; ++j) {
-        const int tid = __ldg(P.ax.tab + b0 + j) & 0xFFFF;
+        const int tid = __ldg(P.ax.tid + b0 + j);
         bulk_g2s(base + P.off_b + j * tile_bytes, P.ax.tiles + static_cast<size_t>(tid) * tile_bytes,
                  tile_bytes, wbar);
       }
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kThreads)
       uint32_t ph = 0;
       const int nslot = (nq + RG::kSteps - 1) / RG::kSteps;
       for (int j = 0; j < nblk; ++j) {
-        const int ws = __ldg(P.ax.tab + b0 + j) >> 16;  // window start (signed)
+        const int ws = __ldg(P.ax.ws + b0 + j);  // window start (may be negative)
         for (int q = 0; q < nslot; ++q) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], RG::kSlot);

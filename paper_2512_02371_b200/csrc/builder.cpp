@@ -206,12 +206,15 @@ static ts_status build_axis_host(int n_in, int n_out, int taps, const int32_t* f
     a->ws[b] = ws[b];
     a->tid[b] = tid[b];
   }
-  if (a->ws[0] < -32768 || a->ws[nb - 1] > 32767 || a->ntiles > 65535)
-    return set_error(TS_ERR_UNSUPPORTED, "axis too long for packed block tables");
-  a->tab.resize(a->ws.size());
-  for (size_t b = 0; b < a->ws.size(); ++b)
-    a->tab[b] = static_cast<int32_t>(static_cast<uint32_t>(a->ws[b]) << 16) |
-                static_cast<int32_t>(a->tid[b] & 0xFFFF);
+  // packed (ws << 16 | tid) tables for the fused kernel's uniform reads; axes
+  // beyond +-32K inputs or 64K distinct tiles run as axis passes, which read
+  // the plain ws / tid arrays
+  a->tab_ok = a->ws[0] >= -32768 && a->ws[nb - 1] <= 32767 && a->ntiles <= 65535;
+  a->tab.assign(a->ws.size(), 0);
+  if (a->tab_ok)
+    for (size_t b = 0; b < a->ws.size(); ++b)
+      a->tab[b] = static_cast<int32_t>(static_cast<uint32_t>(a->ws[b]) << 16) |
+                  static_cast<int32_t>(a->tid[b] & 0xFFFF);
 
   // pass-1 (rows) geometry: 8 blocks per tile
   int rspan = 0;

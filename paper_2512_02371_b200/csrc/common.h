@@ -86,6 +86,7 @@ struct ts_axis {
   int32_t* d_tab = nullptr;
   uint8_t* d_tiles = nullptr;
   std::vector<int32_t> tab;         // packed (ws << 16) | tid, nb + kBlockPad entries
+  bool tab_ok = true;               // packing fits (|ws| < 32K, < 64K tiles)
   mutable tsb::StripPlan* strip[2] = {nullptr, nullptr};  // lazily built per role
 
   tsb::AxisDev dev() const {

@@ -591,6 +591,9 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
   P.trace = g_trace;
   P.trace_ctas = g_trace_ctas;
   P.trace_tiles = g_trace_tiles;
+  if (!ra->tab_ok || !ca->tab_ok)
+    return set_error(TS_ERR_UNSUPPORTED,
+                     "separable: axis longer than the fused kernel's packed block tables (32K)");
   if (ra->K > 256 || ca->K > 256)
     return set_error(TS_ERR_UNSUPPORTED,
                      "separable: windows %d / %d exceed the fused kernel's 256 (use axis passes)",

@@ -92,3 +92,37 @@ def test_run_from_host_matches_device_path():
     torch.cuda.synchronize()
     ref = pipelines.downsample2x(x.cuda()).cpu()
     assert torch.equal(out, ref)
+
+
+def test_very_long_axis():
+    """A 128K-wide axis: beyond the fused kernel's packed block tables (32K
+    inputs), so it runs as axis passes (plain ws / tid tables)."""
+    from paper_2512_02371_b200 import pipelines
+    x = _img((1, 16, 131072), 36)
+    y = _gpu(pipelines.resample, x, out_h=8, out_w=65536)
+    ref = pipelines_ref.resample(x, 8, 65536)
+    assert np.abs(y - ref).max() <= TOL
+
+
+def test_non_contiguous_and_f32_inputs():
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    base = torch.from_numpy(_img((3, 96, 256), 37)).cuda()
+    x = base[:, :, ::2]  # non-contiguous view, 96 x 128
+    y = pipelines.downsample2x(x, out_dtype=torch.float32)
+    ref = pipelines_ref.resample(x.cpu().contiguous().numpy(), 48, 64)
+    assert np.abs(y.cpu().numpy() - ref).max() <= TOL
+    with pytest.raises(TypeError):
+        pipelines.downsample2x(torch.zeros((1, 16, 16), dtype=torch.int32, device="cuda"))
+
+
+def test_fused_kernel_global_block_tables():
+    """> 3072 block-table entries (rows + columns) but < 32K inputs: the fused
+    kernel reads its tables from global memory instead of the parameter bank."""
+    from paper_2512_02371_b200 import axis, pipelines
+    ra, ca = axis.lanczos3(24000, 48000, 0), axis.lanczos3(48, 96, 0)  # 2x up: 3000+ blocks
+    assert ra.info["blocks"] + ca.info["blocks"] + 128 > 3072 and pipelines.fused_supported(ra, ca)
+    x = _img((1, 24000, 48), 38)
+    y = _gpu(pipelines.resample, x, out_h=48000, out_w=96)
+    ref = pipelines_ref.resample(x, 48000, 96)
+    assert np.abs(y - ref).max() <= TOL
