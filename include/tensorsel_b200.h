@@ -263,6 +263,11 @@ TS_API ts_status ts_probe_tma(const void* src, int planes, int H, int W, int row
  * columns of their lane quarter `reps` times with tcgen05.ld.32x32b.x{x}. */
 TS_API ts_status ts_probe_tmem_ld(int x, int warps, int cols, int reps, long long* cycles,
                                   void* stream);
+/* M = 64 accumulator layout probe: D (128 lanes x n, pre-filled with -1) after
+ * one kind::f16 M=64 MMA (A 64 x 16, B 16 x n, row-major f32 in) issued at
+ * TMEM lane lane_base; d receives all 128 lanes. */
+TS_API ts_status ts_probe_m64(const float* a, const float* b, float* d, int n, int lane_base,
+                              void* stream);
 TS_API ts_status ts_probe_issue2(int amode, int bmode, int n, int count, int nacc,
                                  long long* cycles, void* stream);
 

@@ -74,6 +74,7 @@ _SIGNATURES = {
     "ts_strip_info": (_I, [ctypes.POINTER(ctypes.c_int)]),
     "ts_probe_tma": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P]),
     "ts_probe_tmem_ld": (_I, [_I, _I, _I, _I, _P, _P]),
+    "ts_probe_m64": (_I, [_P, _P, _P, _I, _I, _P]),
     "ts_probe_issue2": (_I, [_I, _I, _I, _I, _I, _P, _P]),
     "ts_cast_f32_bf16": (_I, [_P, _P, _I64, _P]),
     "ts_run_conv_group": (_I, [_P, _P]),

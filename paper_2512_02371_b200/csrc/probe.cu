@@ -635,3 +635,91 @@ extern "C" ts_status ts_probe_tmem_ld(int x, int warps, int cols, int reps, long
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_tmem_ld launch");
 }
+
+// M = 64 layout probe: D (TMEM, pre-filled with -1) = A (64 x 16, K-major core
+// matrices) x B (16 x n, K-major), kind::f16, issued at TMEM lane `lane_base`
+// (0 or 64).  Dumps all 128 lanes x n columns so the caller sees where an
+// M = 64 accumulator lands.
+namespace tsb {
+__global__ void __launch_bounds__(128, 1)
+    probe_m64_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ d,
+                     int n, int lane_base) {
+  __shared__ __align__(1024) uint8_t sm[64 * 32 + 256 * 32 + 64];
+  uint8_t* sa = sm;
+  uint8_t* sb = sm + 64 * 32;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 64 * 32 + 256 * 32);
+  __shared__ uint32_t slot;
+  for (int e = threadIdx.x; e < 64 * 16; e += blockDim.x) {
+    const int m = e / 16, kk = e % 16;
+    *reinterpret_cast<__nv_bfloat16*>(sa + (m / 8) * 256 + (kk / 8) * 128 + (m % 8) * 16 + (kk % 8) * 2) =
+        __float2bfloat16_rn(a[e]);
+  }
+  for (int e = threadIdx.x; e < 16 * n; e += blockDim.x) {
+    const int kk = e / n, nn = e % n;
+    *reinterpret_cast<__nv_bfloat16*>(sb + (nn / 8) * 256 + (kk / 8) * 128 + (nn % 8) * 16 + (kk % 8) * 2) =
+        __float2bfloat16_rn(b[e]);
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) tmem_alloc<256>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const uint32_t tl = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  {
+    uint32_t r[16];
+    for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(-1.0f);
+    for (int c = 0; c < n; c += 16)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+          "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tl + c),
+          "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+          "r"(r[15])
+          : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc(kFmtBF16, 64, n, 0, 0);
+    const uint64_t ad = make_sdesc(smem_u32(sa), 128u, 256u, kSwizzleNone);
+    const uint64_t bd = make_sdesc(smem_u32(sb), 128u, 256u, kSwizzleNone);
+    mma_f16_ss(tmem + (static_cast<uint32_t>(lane_base) << 16), ad, bd, idesc, 0u);
+    mma_commit(bar);
+  }
+  __syncwarp();
+  mbar_wait(bar, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  for (int c = 0; c < n; c += 16) {
+    uint32_t r[16];
+    tmem_ld16(tl + c, r);
+    tmem_wait_ld();
+    for (int i = 0; i < 16; ++i) d[row * n + c + i] = __uint_as_float(r[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+}  // namespace tsb
+
+extern "C" ts_status ts_probe_m64(const float* a, const float* b, float* d, int n, int lane_base,
+                                  void* stream) {
+  using namespace tsb;
+  if (!a || !b || !d || n < 16 || n > 256 || n % 16 || (lane_base != 0 && lane_base != 64 &&
+                                                         lane_base != 32 && lane_base != 96))
+    return set_error(TS_ERR_INVALID, "probe_m64: bad arguments");
+  probe_m64_kernel<<<1, 128, 0, static_cast<cudaStream_t>(stream)>>>(a, b, d, n, lane_base);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_m64 launch");
+}
