@@ -70,12 +70,33 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 // Wait for the phase with the given parity to complete.  A pipeline bug must
 // not wedge the GPU: after ~4 s of waiting the kernel traps (the launch then
 // fails with an error the host reports instead of hanging the box).
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the
+// phase completes (or ~0.1 ms elapse) instead of spinning; spinning waiters
+// took half the issue slots of the DCT kernel (BRA/SYNCS/YIELD in ncu).
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(100000u)
+      : "memory");
+  return ok != 0;
+}
+
+// The timer is read once per 1024 polls in an outer loop: written as one
+// loop with `(++n & 1023) == 0 && timer...`, ptxas evaluates the %globaltimer
+// read (CS2R) on every poll, and the polling warps then saturate the XU pipe
+// the kernels' F2FP conversions need (ncu: XU 94% busy in the DCT kernel).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = global_timer_ns();
-  uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && global_timer_ns() - t0 > 4000000000ull) __trap();
+  for (;;) {
+#pragma unroll 1
+    for (int i = 0; i < 1024; ++i)
+      if (mbar_try_wait_sleep(bar, parity)) return;
+    if (global_timer_ns() - t0 > 4000000000ull) __trap();
   }
 }
 
