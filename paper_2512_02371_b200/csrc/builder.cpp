@@ -287,6 +287,12 @@ void ts_axis_destroy(ts_axis* a) {
     if (sp->d_specials) cudaFree(sp->d_specials);
     delete sp;
   }
+  for (auto* m : a->merged) {
+    if (!m) continue;
+    if (m->d_tab) cudaFree(m->d_tab);
+    if (m->d_tiles) cudaFree(m->d_tiles);
+    delete m;
+  }
   if (a->d_tiles) cudaFree(a->d_tiles);
   delete a;
 }

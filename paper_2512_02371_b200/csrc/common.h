@@ -39,6 +39,18 @@ struct AxisDev {
 }  // namespace tsb
 
 namespace tsb {
+constexpr int kMaxMerge = 8;  // 16-output blocks per super-block (merge.cpp)
+
+// Super-block form of an axis (csrc/merge.cpp): m blocks -> one N = 16m block.
+struct MergedAxis {
+  bool ok = false;
+  int m = 1, K = 0, tile_bytes = 0, ng = 0, ntiles = 0;
+  std::vector<int32_t> ws, tid, tab;  // per super-block (padding included)
+  std::vector<uint16_t> tiles;        // ntiles x (K x 16m) bf16, K-major core matrices
+  int32_t* d_tab = nullptr;
+  uint8_t* d_tiles = nullptr;
+};
+
 // Shift-invariant "strip" form of an axis for the v5 separable kernel
 // (csrc/strip.cpp): per tile, K-step q's operand slice equals a fixed strip
 // shifted by `shift` outputs per 16 inputs, except a few edge slices.
@@ -88,6 +100,7 @@ struct ts_axis {
   std::vector<int32_t> tab;         // packed (ws << 16) | tid, nb + kBlockPad entries
   bool tab_ok = true;               // packing fits (|ws| < 32K, < 64K tiles)
   mutable tsb::StripPlan* strip[2] = {nullptr, nullptr};  // lazily built per role
+  mutable tsb::MergedAxis* merged[tsb::kMaxMerge + 1] = {};  // lazily built per factor
 
   tsb::AxisDev dev() const {
     return tsb::AxisDev{d_ws, d_tid, d_tab, d_tiles, K, nb, tile_bytes, ntiles};

@@ -38,6 +38,8 @@
 
 namespace tsb {
 
+const MergedAxis* axis_merged(const ts_axis* a, int m);
+int choose_merge(const ts_axis* a, int blocks);
 ts_status strip_run(const ts_axis* ra, const ts_axis* ca, int planes, const void* in, int64_t in_rs,
                     int64_t in_ps, void* out, int64_t out_rs, int64_t out_ps, int out_dtype,
                     cudaStream_t stream, bool dry);
@@ -64,6 +66,8 @@ struct SepParams {
   AxisDev r;  // rows axis (pass 1)
   AxisDev c;  // cols axis (pass 2)
   int nb2;    // column blocks per tile
+  int m1, m2;    // merge factors: blocks per super-block (csrc/merge.cpp), rows / cols
+  int sb1, sb2;  // super-blocks per tile: 8 / m1 (pass 1), nb2 / m2 (pass 2)
   int R1;     // staged input rows per tile (multiple of 16)
   int nrt, nct, planes, ntiles;
   unsigned long long* trace;  // diagnostics: per-(CTA, tile, event) clock64 stamps or null
@@ -193,7 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nb2 = P.nb2;
   const int nst = static_cast<int>(L.nst);
   const int nmid = static_cast<int>(L.nmid);
-  const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, /*a MN-major*/ 1, /*b K-major*/ 0);
+  // N = 16 x merge factor (super-blocks of m 16-output blocks)
+  const uint32_t idesc1 = make_idesc(kFmtBF16, 128, 16 * P.m1, /*a MN-major*/ 1, /*b K-major*/ 0);
+  const uint32_t idesc2 = make_idesc(kFmtBF16, 128, 16 * P.m2, /*a MN-major*/ 1, /*b K-major*/ 0);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -210,14 +216,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
         const int s = it % nst;
         const uint32_t ph = (it / nst) & 1;
-        const int b1 = tw.rt * kRowBlocksPerTile, b2 = tw.ct * nb2;
+        const int b1 = tw.rt * P.sb1, b2 = tw.ct * P.sb2;
         const int row0 = tab_ws(tab_r(P, b1)), col0 = tab_ws(tab_c(P, b2));
         uint32_t wbytes = 0;
         if (!L.resident) {
-          for (int k = 0; k < kRowBlocksPerTile; ++k)
+          for (int k = 0; k < P.sb1; ++k)
             if (k == 0 || tab_tid(tab_r(P, b1 + k)) != tab_tid(tab_r(P, b1 + k - 1)))
               wbytes += P.r.tile_bytes;
-          for (int j = 0; j < nb2; ++j)
+          for (int j = 0; j < P.sb2; ++j)
             if (j == 0 || tab_tid(tab_c(P, b2 + j)) != tab_tid(tab_c(P, b2 + j - 1)))
               wbytes += P.c.tile_bytes;
         }
@@ -232,14 +238,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(dst + P.R1 * 128 + hr * 128, &tm_in, &full[s], col0 + 64, row0 + hr, tw.p);
         if (!L.resident) {
           uint8_t* wd = base + L.off_w + s * L.w_stage;
-          for (int k = 0; k < kRowBlocksPerTile; ++k) {
+          for (int k = 0; k < P.sb1; ++k) {
             const int tid = tab_tid(tab_r(P, b1 + k));
             if (k == 0 || tid != tab_tid(tab_r(P, b1 + k - 1)))
               bulk_g2s(wd + k * P.r.tile_bytes,
                        P.r.tiles + static_cast<size_t>(tid) * P.r.tile_bytes, P.r.tile_bytes,
                        &full[s]);
           }
-          for (int j = 0; j < nb2; ++j) {
+          for (int j = 0; j < P.sb2; ++j) {
             const int tid = tab_tid(tab_c(P, b2 + j));
             if (j == 0 || tid != tab_tid(tab_c(P, b2 + j - 1)))
               bulk_g2s(wd + L.w1_bytes + j * P.c.tile_bytes,
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
       const int s = it % nst;
       const int d = it & 1;
-      const int b1 = tw.rt * kRowBlocksPerTile;
+      const int b1 = tw.rt * P.sb1;
       const int row0 = tab_ws(tab_r(P, b1));
       const uint32_t a0 = base_s + s * L.in_stage;
       const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
@@ -272,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int slot = 0, prev = -1;
 #pragma unroll
       for (int k = 0; k < kRowBlocksPerTile; ++k) {
+        if (k >= P.sb1) break;
         const int32_t e = tab_r(P, b1 + k);
         const int tid = tab_tid(e);
         if (L.resident)
@@ -282,12 +289,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t ad = make_sdesc(a0 + static_cast<uint32_t>(tab_ws(e) - row0) * 128u, lbo_in,
                                        1024u, kSwizzle128B);
         const uint64_t bd = make_sdesc(w0 + slot * tb1, 128u, sbo1, kSwizzleNone);
-        const uint32_t dcol = tmem + d * 128u + 16u * k;
+        const uint32_t dcol = tmem + d * 128u + static_cast<uint32_t>(16 * P.m1 * k);
 #pragma unroll
         for (int q = 0; q < (KQ1 > 0 ? KQ1 : 16); ++q) {
           if (KQ1 == 0 && q >= kq1) break;
           // +2048 B (16 rows of A) and +256 B (two k-chunks of B) per K step
-          mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc, q > 0 ? 1u : 0u);
+          mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc1, q > 0 ? 1u : 0u);
         }
       }
       mma_commit_elect(&dv_full[d]);
@@ -304,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
       const int s = it % nst;
       const int m = it % nmid;
-      const int b2 = tw.ct * nb2;
+      const int b2 = tw.ct * P.sb2;
       const int col0 = tab_ws(tab_c(P, b2));
       const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
       const uint32_t mid_s = base_s + L.off_mid + m * kMidBytes;
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       int slot = 0, prev = -1;
 #pragma unroll 1
-      for (int j = 0; j < nb2; ++j) {
+      for (int j = 0; j < P.sb2; ++j) {
         const int32_t e = tab_c(P, b2 + j);
         const int tid = tab_tid(e);
         if (L.resident)
@@ -326,11 +333,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t ad = make_sdesc(mid_s + static_cast<uint32_t>((tab_ws(e) - col0) / 8) * 1024u,
                                        16384u, 1024u, kSwizzle128B);
         const uint64_t bd = make_sdesc(w0 + L.w1_bytes + slot * tb2, 128u, sbo2, kSwizzleNone);
-        const uint32_t dcol = tmem + 256u + 16u * j;
+        const uint32_t dcol = tmem + 256u + static_cast<uint32_t>(16 * P.m2 * j);
 #pragma unroll
         for (int q = 0; q < (KQ2 > 0 ? KQ2 : 16); ++q) {
           if (KQ2 == 0 && q >= kq2) break;
-          mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc, q > 0 ? 1u : 0u);
+          mma_f16_ss_elect(dcol, ad + 128u * q, bd + 16u * q, idesc2, q > 0 ? 1u : 0u);
         }
       }
       mma_commit_elect(dh_full);
@@ -493,8 +500,8 @@ static bool plan_smem(SepParams& P, int oes) {
   const uint32_t tb1 = P.r.tile_bytes, tb2 = P.c.tile_bytes;
   const uint32_t res_w1 = align_up(static_cast<uint32_t>(P.r.ntiles) * tb1, 128);
   const uint32_t res_bytes = align_up(res_w1 + static_cast<uint32_t>(P.c.ntiles) * tb2, 1024);
-  const uint32_t st_w1 = kRowBlocksPerTile * tb1;
-  const uint32_t st_bytes = align_up(st_w1 + P.nb2 * tb2, 1024);
+  const uint32_t st_w1 = static_cast<uint32_t>(P.sb1) * tb1;
+  const uint32_t st_bytes = align_up(st_w1 + static_cast<uint32_t>(P.sb2) * tb2, 1024);
   const uint32_t out_bytes = align_up(128u * P.nb2 * 16u * oes, 1024);
   const uint32_t fixed = out_bytes + 256 + 1024;  // barriers + alignment slack
   // (a single input stage was measured slower than two axis passes: 2048^2 ->
@@ -556,6 +563,7 @@ static ts_status launch_sep_k2(const SepParams& P, const CUtensorMap& tin,
     case 2: return launch_sep_k<OutT, KQ1, 2>(P, tin, tout, stream);
     case 3: return launch_sep_k<OutT, KQ1, 3>(P, tin, tout, stream);
     case 4: return launch_sep_k<OutT, KQ1, 4>(P, tin, tout, stream);
+    case 5: return launch_sep_k<OutT, KQ1, 5>(P, tin, tout, stream);
     default: return launch_sep_k<OutT, KQ1, 0>(P, tin, tout, stream);
   }
 }
@@ -567,6 +575,8 @@ static ts_status launch_sep(const SepParams& P, const CUtensorMap& tin, const CU
     case 2: return launch_sep_k2<OutT, 2>(P, tin, tout, stream);
     case 3: return launch_sep_k2<OutT, 3>(P, tin, tout, stream);
     case 4: return launch_sep_k2<OutT, 4>(P, tin, tout, stream);
+    case 5: return launch_sep_k2<OutT, 5>(P, tin, tout, stream);
+    case 6: return launch_sep_k2<OutT, 6>(P, tin, tout, stream);
     default: return launch_sep_k2<OutT, 0>(P, tin, tout, stream);
   }
 }
@@ -604,24 +614,51 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
   if (ca->col_nbt < 1)
     return set_error(TS_ERR_UNSUPPORTED, "cols axis: window %d does not fit a 128-column tile",
                      ca->K);
-  P.r = ra->dev();
-  P.c = ca->dev();
+  auto dev_of = [](const ts_axis* a, int m) {
+    if (m <= 1) return a->dev();
+    const MergedAxis* M = axis_merged(a, m);
+    return AxisDev{nullptr, nullptr, M->d_tab, M->d_tiles, M->K, M->ng, M->tile_bytes, M->ntiles};
+  };
+  auto tab_of = [](const ts_axis* a, int m) -> const std::vector<int32_t>& {
+    return m <= 1 ? a->tab : axis_merged(a, m)->tab;
+  };
+  P.m1 = choose_merge(ra, kRowBlocksPerTile);
+  P.sb1 = kRowBlocksPerTile / P.m1;
+  P.r = dev_of(ra, P.m1);
   P.R1 = ra->row_span;
   P.nrt = (ra->nb + kRowBlocksPerTile - 1) / kRowBlocksPerTile;
   P.planes = planes;
-  const int ntr = static_cast<int>(ra->tab.size()), ntc = static_cast<int>(ca->tab.size());
-  P.ptab = (ntr + ntc <= kParamTab) ? 1 : 0;
-  P.ptab_c = ntr;
-  if (P.ptab) {
-    for (int i = 0; i < ntr; ++i) P.tab[i] = ra->tab[i];
-    for (int i = 0; i < ntc; ++i) P.tab[ntr + i] = ca->tab[i];
-  }
-  // widest column tile (most output blocks per staged V tile) that fits smem
+  // widest column tile (most output blocks per staged V tile) that fits
+  // smem; at each width try the chosen super-block merges first, then
+  // unmerged axes (merged tiles are larger and may not fit resident)
+  const int m1_best = P.m1;
   for (int nb2 = ca->col_nbt; nb2 >= 1; --nb2) {
-    P.nb2 = nb2;
-    P.nct = (ca->nb + nb2 - 1) / nb2;
-    P.ntiles = planes * P.nrt * P.nct;
-    if (plan_smem(P, oes)) return TS_OK;
+    const int m2_best = choose_merge(ca, nb2);
+    for (int variant = 0; variant < 3; ++variant) {
+      const int m1 = variant == 2 ? 1 : m1_best;
+      const int m2 = variant >= 1 ? 1 : m2_best;
+      if (variant > 0 && m1 == m1_best && m2 == m2_best) continue;
+      if (variant == 2 && m1_best == 1) continue;
+      P.m1 = m1;
+      P.sb1 = kRowBlocksPerTile / m1;
+      P.r = dev_of(ra, m1);
+      P.nb2 = nb2;
+      P.m2 = m2;
+      P.sb2 = nb2 / m2;
+      P.c = dev_of(ca, m2);
+      const std::vector<int32_t>& tr = tab_of(ra, m1);
+      const std::vector<int32_t>& tc = tab_of(ca, m2);
+      const int ntr = static_cast<int>(tr.size()), ntc = static_cast<int>(tc.size());
+      P.ptab = (ntr + ntc <= kParamTab) ? 1 : 0;
+      P.ptab_c = ntr;
+      if (P.ptab) {
+        for (int i = 0; i < ntr; ++i) P.tab[i] = tr[i];
+        for (int i = 0; i < ntc; ++i) P.tab[ntr + i] = tc[i];
+      }
+      P.nct = (ca->nb + nb2 - 1) / nb2;
+      P.ntiles = planes * P.nrt * P.nct;
+      if (plan_smem(P, oes)) return TS_OK;
+    }
   }
   return set_error(TS_ERR_UNSUPPORTED, "separable: tile (R1=%d) does not fit smem", P.R1);
 }

@@ -12,3 +12,8 @@ for t in (9, 15, 21, 31):
     k = filters.gaussian_taps(t)
     show(f"gauss{t}", axis.convolution(4320, k, 0), axis.convolution(7680, k, 0), 48)
 show("up2x", axis.lanczos3(1080, 2160, 0), axis.lanczos3(1920, 3840, 0), 24)
+from paper_2512_02371_b200 import axis as _ax
+from oracle import pipelines_ref as _pr
+ra = _ax.resample_filter(2160, 1080, filters.gaussian_taps(9), 0)
+ca = _ax.resample_filter(3840, 1920, filters.gaussian_taps(9), 0)
+show("c5 composed", ra, ca, 48)
