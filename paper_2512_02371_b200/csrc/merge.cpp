@@ -106,6 +106,8 @@ static double operand_bytes(int K, int blocks, int m) {
 
 int choose_merge(const ts_axis* a, int blocks) {
   if (std::getenv("TSB_NO_MERGE")) return 1;
+  const char* th = std::getenv("TSB_MERGE_GAIN");  // required saving (default 0.05)
+  const double keep = 1.0 - (th ? std::atof(th) : 0.05);
   int best = 1;
   double best_cost = operand_bytes(a->K, blocks, 1);
   for (int m = 2; m <= kMaxMerge && m <= blocks; ++m) {
@@ -113,7 +115,7 @@ int choose_merge(const ts_axis* a, int blocks) {
     const MergedAxis* M = axis_merged(a, m);
     if (!M || !M->ok || M->K > 256) continue;
     const double c = operand_bytes(M->K, blocks, m);
-    if (c < 0.9 * best_cost) {  // only merge for a clear (>= 10%) saving
+    if (c < keep * best_cost) {  // only merge for a clear saving
       best = m;
       best_cost = c;
     }
