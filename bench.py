@@ -266,6 +266,7 @@ def run_b200(args):
     e2e_ms = float(e2e_ms[0])
 
     peak, peak_kind = measured_peaks()
+    launches_per_step = 1
     if op == "dct16":
         kernel_name = "tsb::dct::dct16_kernel (fused DCT-16 denoise)"
     else:
@@ -275,6 +276,7 @@ def run_b200(args):
         kernel_name = ("tsb::separable_kernel (fused V+H tcgen05 pass)" if fused else
                        "tsb::axis_pass_kernel x2 (vertical + horizontal, bf16 intermediate; "
                        "alg bytes exclude the intermediate)")
+        launches_per_step = (1 if fused else 2) + (1 if in_dtype == torch.float32 else 0)
     alg_bytes = in_bytes + out_bytes  # per launch per GPU
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
@@ -320,7 +322,7 @@ def run_b200(args):
                     "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out_bytes,
                     "api": "paper_2512_02371_b200.pipelines.run_from_host (pinned host -> device -> "
                            "host, copies overlapped with kernels over 3 streams)"},
-            "gpu_launches": K,
+            "gpu_launches": K * launches_per_step,  # incl. the f32->bf16 cast kernel (c1)
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
