@@ -277,6 +277,8 @@ def run_b200(args):
                        "tsb::axis_pass_kernel x2 (vertical + horizontal, bf16 intermediate; "
                        "alg bytes exclude the intermediate)")
         launches_per_step = (1 if fused else 2) + (1 if in_dtype == torch.float32 else 0)
+        if in_dtype == torch.float32:
+            kernel_name = "f32->bf16 cast kernel + " + kernel_name + " (timed together)"
     alg_bytes = in_bytes + out_bytes  # per launch per GPU
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
