@@ -426,6 +426,55 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t tl = tmem + lane_off;
     const int et = threadIdx.x - 64;
+    auto do_e4 = [&](int it4, int X4, int Y4, int p4) {
+        // ---- E4: D4 (lane = band row r, columns = band column c) -> output block
+        // (S7 completes twice per band; E4 waits the second: parity 1)
+        mbar_wait(s7done, 1u);
+        tc_fence_after();
+        if (et == 0) stamp(P, it4, 22);
+        if (sp == 0) dbg_dump(P, it4, 3, 0, tl + kTD4, row, BW);
+        if (et == 0) bulk_wait_read0();
+        named_bar_sync(1, kEpiThreads);
+        {
+          uint32_t v[2][16];
+          tmem_ld16(tl + kTD4 + 32u * sp, v[0]);
+          tmem_ld16(tl + kTD4 + 32u * sp + 16u, v[1]);
+          tmem_wait_ld();
+          tc_fence_before();
+          warp_arrive(e4, lane);
+          if (row >= 8 && row < 8 + kOutRows) {
+            uint8_t* orow = base + kOffOut + (row - 8) * kOut * sizeof(OutT);
+            // band columns 8..BW-9 -> output columns 0..kOut-1, 8 at a time
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int c = 32 * sp + 8 * g;
+              if (c >= 8 && c < 8 + kOut) {
+                const uint32_t* src = &v[g >> 1][8 * (g & 1)];
+                if constexpr (sizeof(OutT) == 2) {
+                  *reinterpret_cast<uint4*>(orow + (c - 8) * 2) =
+                      make_uint4(pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1])),
+                                 pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3])),
+                                 pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5])),
+                                 pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7])));
+                } else {
+                  *reinterpret_cast<uint4*>(orow + (c - 8) * 4) =
+                      make_uint4(src[0], src[1], src[2], src[3]);
+                  *reinterpret_cast<uint4*>(orow + (c - 8) * 4 + 16) =
+                      make_uint4(src[4], src[5], src[6], src[7]);
+                }
+              }
+            }
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, kEpiThreads);
+        if (et == 0) {
+          tma_store_3d(&tm_out, base + kOffOut, X4, Y4, p4);
+          bulk_commit();
+          stamp(P, it4, 23);
+        }
+    };
+    int pX = 0, pY = 0, pP = 0, pit = -1;  // band whose E4 is pending
     int it = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
@@ -455,6 +504,10 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         tc_fence_before();
         warp_arrive(c1, lane);
         if (et == 0) stamp(P, it, 12 * p + 1);
+        if (p == 0 && pit >= 0) {
+          do_e4(pit, pX, pY, pP);
+          pit = -1;
+        }
         // ---- E2: coring of D2 (lane f, columns 16*(kNq0*q+j) + l) in place,
         // one column phase at a time
         const bool dc_row = (row & 15) == 0;
@@ -525,52 +578,11 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         if (et == 0) stamp(P, it, 12 * p + 5);
         ph ^= 1;
       }
-      // ---- E4: D4 (lane = band row r, columns = band column c) -> output block
-      mbar_wait(s7done, ph ^ 1);
-      tc_fence_after();
-      if (et == 0) stamp(P, it, 22);
-      if (sp == 0) dbg_dump(P, it, 3, 0, tl + kTD4, row, BW);
-      if (et == 0) bulk_wait_read0();
-      named_bar_sync(1, kEpiThreads);
-      {
-        uint32_t v[2][16];
-        tmem_ld16(tl + kTD4 + 32u * sp, v[0]);
-        tmem_ld16(tl + kTD4 + 32u * sp + 16u, v[1]);
-        tmem_wait_ld();
-        tc_fence_before();
-        warp_arrive(e4, lane);
-        if (row >= 8 && row < 8 + kOutRows) {
-          uint8_t* orow = base + kOffOut + (row - 8) * kOut * sizeof(OutT);
-          // band columns 8..BW-9 -> output columns 0..kOut-1, 8 at a time
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const int c = 32 * sp + 8 * g;
-            if (c >= 8 && c < 8 + kOut) {
-              const uint32_t* src = &v[g >> 1][8 * (g & 1)];
-              if constexpr (sizeof(OutT) == 2) {
-                *reinterpret_cast<uint4*>(orow + (c - 8) * 2) =
-                    make_uint4(pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1])),
-                               pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3])),
-                               pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5])),
-                               pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7])));
-              } else {
-                *reinterpret_cast<uint4*>(orow + (c - 8) * 4) =
-                    make_uint4(src[0], src[1], src[2], src[3]);
-                *reinterpret_cast<uint4*>(orow + (c - 8) * 4 + 16) =
-                    make_uint4(src[4], src[5], src[6], src[7]);
-              }
-            }
-          }
-        }
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(1, kEpiThreads);
-      if (et == 0) {
-        tma_store_3d(&tm_out, base + kOffOut, X, Y, R.p);
-        bulk_commit();
-        stamp(P, it, 23);
-      }
+      // E4 of this band runs during the next band's first row phase (after
+      // its C1), off the critical path; the last band's after the loop
+      pX = X; pY = Y; pP = R.p; pit = it;
     }
+    if (pit >= 0) do_e4(pit, pX, pY, pP);
     if (et == 0) bulk_wait0();
   }
   tc_fence_before();
@@ -714,14 +726,14 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
     e = cudaMemcpy(d_consts[dev], h, dct::kConstBytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_error(e, "dct16 consts copy");
   }
-  // band width: 64 columns (two CTAs per SM overlap one band's MMAs with the
-  // other's TMEM epilogues) unless TSB_DCT_BAND=128
+  // band width: 128 columns (one CTA per SM) unless TSB_DCT_BAND=64 (two
+  // CTAs per SM; within 1% since E4 moved off the critical path)
   const char* v = std::getenv("TSB_DCT_BAND");
-  if (v && std::atoi(v) == 128)
-    return dct16_run_bw<128>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
-                             threshold, soft, d_consts[dev], stream);
-  return dct16_run_bw<64>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
-                          threshold, soft, d_consts[dev], stream);
+  if (v && std::atoi(v) == 64)
+    return dct16_run_bw<64>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
+                            threshold, soft, d_consts[dev], stream);
+  return dct16_run_bw<128>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
+                           threshold, soft, d_consts[dev], stream);
 }
 
 }  // namespace tsb
