@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 
 def build(verbose: bool = False) -> str:
     os.makedirs(os.path.join(HERE, "_native"), exist_ok=True)
-    cmd = ["make", "-C", CSRC]
+    cmd = ["make", "-j", str(min(16, os.cpu_count() or 1)), "-C", CSRC]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode:
         sys.stdout.write(r.stdout)
