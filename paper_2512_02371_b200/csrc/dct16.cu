@@ -37,6 +37,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "common.h"
 #include "sm100.cuh"
@@ -715,16 +716,25 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
       (out_rs * oes) % 16 || out_ps < out_rs * H || (out_ps * oes) % 16)
     return set_error(TS_ERR_INVALID, "dct16: strides");
   static uint8_t* d_consts[64] = {nullptr};
+  static std::mutex consts_mu;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return set_error(TS_ERR_INVALID, "dct16: device index");
-  if (!d_consts[dev]) {
-    uint8_t h[dct::kConstBytes] = {0};
-    build_consts(h);
-    cudaError_t e = cudaMalloc(&d_consts[dev], dct::kConstBytes);
-    if (e != cudaSuccess) return cuda_error(e, "dct16 consts");
-    e = cudaMemcpy(d_consts[dev], h, dct::kConstBytes, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_error(e, "dct16 consts copy");
+  {
+    std::lock_guard<std::mutex> lock(consts_mu);  // first call per device uploads once
+    if (!d_consts[dev]) {
+      uint8_t h[dct::kConstBytes] = {0};
+      build_consts(h);
+      uint8_t* d = nullptr;
+      cudaError_t e = cudaMalloc(&d, dct::kConstBytes);
+      if (e != cudaSuccess) return cuda_error(e, "dct16 consts");
+      e = cudaMemcpy(d, h, dct::kConstBytes, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_error(e, "dct16 consts copy");
+      }
+      d_consts[dev] = d;
+    }
   }
   // band width: 128 columns (one CTA per SM) unless TSB_DCT_BAND=64 (two
   // CTAs per SM; within 1% since E4 moved off the critical path)
