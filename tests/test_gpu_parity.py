@@ -198,3 +198,26 @@ def test_paper_table_921():
     y = _gpu(pipelines.resample, x, out_h=921, out_w=921, out_dtype=torch.float32)
     ref = pipelines_ref.resample(x, 921, 921)
     assert np.abs(y - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("taps", [101, 255])
+def test_very_wide_box_blur_two_pass(taps):
+    """Box filters wider than the fused column tile run as axis passes."""
+    import torch
+    from paper_2512_02371_b200 import axis, filters, pipelines
+    x = _img((1, 300, 520), 25)
+    k = filters.box_taps(taps)
+    assert not pipelines.fused_supported(axis.convolution(300, k, 0), axis.convolution(520, k, 0))
+    y = _gpu(pipelines.box_blur, x, taps=taps, out_dtype=torch.float32)
+    ref = pipelines_ref.box_blur(x, taps)
+    assert np.abs(y - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("shape,oh,ow", [((2, 90, 120), 270, 360), ((1, 64, 80), 200, 150)])
+def test_upsample_3x_and_non_integer(shape, oh, ow):
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = _img(shape, 26)
+    y = _gpu(pipelines.resample, x, out_h=oh, out_w=ow, out_dtype=torch.float32)
+    ref = pipelines_ref.resample(x, oh, ow)
+    assert np.abs(y - ref).max() <= TOL
