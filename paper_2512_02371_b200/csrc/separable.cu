@@ -13,11 +13,14 @@
 //  warp 0      TMA producer: the input halo tile (R1 rows x 128 cols bf16,
 //              128B-swizzled, 4 boxes) into an nst-deep ring; B tiles are
 //              either CTA-resident (copied once) or staged per tile.
-//  warp 1      pass-1 MMA issuer (vertical), per 16-output-row block k:
-//                D_V[c, 16k..] = Σ_r X[r, c] · R_kᵀ[r, ·]   M=128 cols, N=16
+//  warp 1      pass-1 MMA issuer (vertical), per super-block k of m1
+//              16-output-row blocks (merge.cpp; m1 = 1 unless overlapping
+//              windows make merging cheaper):
+//                D_V[c, 16·m1·k..] = Σ_r X[r, c] · R_kᵀ[r, ·]   M=128 cols, N=16·m1
 //                A = staged tile (MN-major SW128), B = R tile (K-major)
-//  warp 10     pass-2 MMA issuer (horizontal), per 16-output-column block j:
-//                D_H[i, 16j..] = Σ_c V[i, c] · C_jᵀ[c, ·]   M=128 rows, N=16
+//  warp 10     pass-2 MMA issuer (horizontal), per super-block j of m2
+//              16-output-column blocks (nb2 <= 16 blocks per tile):
+//                D_H[i, 16·m2·j..] = Σ_c V[i, c] · C_jᵀ[c, ·]   M=128 rows, N=16·m2
 //                A = V (bf16 MN-major SW128, written by warps 2-5)
 //  warps 2-5   epilogue 1: D_V (TMEM) -> bf16 -> V operand (smem, x nmid)
 //  warps 6-9   epilogue 2: D_H (TMEM) -> cast -> smem -> TMA store
@@ -29,6 +32,8 @@
 // TMEM (512 cols): D_V double-buffered at [0,128) and [128,256), D_H at
 // [256, 256 + nb2·16).  Window starts are multiples of 8 rows/cols (the
 // builder guarantees it) so every MMA operand starts on a 1024-byte atom.
+// Waiting warps sleep in mbarrier.try_wait (sm100.cuh) rather than spin:
+// under the sustained power cap that keeps ~70 MHz more SM clock.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
