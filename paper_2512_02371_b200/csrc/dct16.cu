@@ -17,19 +17,25 @@
 //   C1  D1 -> bf16 hi/lo pairs, in TMEM (no shared-memory round trip)
 //   S3  (TS bf16, N=16)   D2[f][16(8q+j)+l] = Σ_c D1[f][16j+8q+c] Dw[l][c]
 //         (hi·hi + lo·hi + hi·lo), A read from TMEM
-//   E2  coring of D2 in place (DC kept)
-//   S5  (TS tf32, N=16)   D3[f][16j+8q+c] (+)= Σ_l D2'[f][..+l] Dw[l][c]
-//   E3  D3 -> B7 (bf16 hi/lo, MN-major: K = f, N = c) in shared memory
-//   S7  (SS bf16, N=128)  D4[r][c] += Σ_f T_pᵀ[r][f] B7[f][c]   (both p accumulate)
+//   E2  coring of D2 (DC kept) -> fp16 pairs in place
+//   S5  (TS f16, N=16)    D3[f][16j+8q+c] (+)= Σ_l D2'[f][..+l] Dw[l][c]
+//   E3  D3 -> B7 (fp16, MN-major: K = f, N = c) in shared memory
+//   S7  (SS f16, N=128)   D4[r][c] += Σ_f T_pᵀ[r][f] B7[f][c]   (both p accumulate)
 //   E4  D4 (lane = band row) -> output block, one TMA store
+//
+// Precision: the forward chain decides coring, so its f32 intermediates
+// travel as bf16 hi/lo pairs (~16 mantissa bits; kind::tf32 does not accept
+// an MN-major A from shared memory on sm_100a — it silently yields zeros, see
+// ts_probe_mma amode 3).  The inverse chain is linear and only has to meet
+// the output tolerance: one fp16 operand per step (11 bits; max error ~1e-3
+// against the f32 oracle, tools/sim_dct_precision.py), half the MMAs and
+// conversions of hi/lo.
 //
 // Clamp-to-edge: TMA zero-fills samples outside the image; for bands on an
 // image border the loader warp replicates the edge row / column into the 8
 // samples beyond it inside the staged band (equivalent to folding the
 // outside weights onto the edge sample), so the transforms have no edge
-// variants.  (kind::tf32 does not accept an MN-major A from shared memory on
-// sm_100a — it silently yields zeros, see ts_probe_mma amode 3 — so f32
-// intermediates travel as bf16 hi/lo pairs, ~16 mantissa bits.)
+// variants.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -80,9 +86,9 @@ struct Geo {
   static constexpr int kChunks = kNq0 + kNq1;                // 16-column chunks of D2
   static constexpr uint32_t kBandBytes = kBandRows * BW * 2;  // BW/64 SW128 boxes
   static constexpr uint32_t kOffX = 0;                        // 2 band buffers
-  static constexpr uint32_t kB7Lo = kBandRows * BW * 2;       // S7 B operand hi, lo
+  static constexpr uint32_t kB7Bytes = kBandRows * BW * 2;    // S7 B operand (fp16)
   static constexpr uint32_t kOffB7 = 2 * kBandBytes;
-  static constexpr uint32_t kOffOut = kOffB7 + 2 * kB7Lo;     // staging (f32 worst case)
+  static constexpr uint32_t kOffOut = kOffB7 + kB7Bytes;      // staging (f32 worst case)
   static constexpr uint32_t kOffC = kOffOut + round1k(kOutRows * kOutW * 4);
   static constexpr uint32_t kOffBar = kOffC + kConstBytes;
   static constexpr uint32_t kSmem = kOffBar + 256 + 1024;
@@ -125,15 +131,6 @@ __device__ __forceinline__ void dbg_dump(const Params& P, int it, int stage, int
   }
 }
 
-__device__ __forceinline__ void mma_tf32_ts_elect(uint32_t d, uint32_t a_tmem, uint64_t b,
-                                                  uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
 __device__ __forceinline__ void mma_f16_ts_elect(uint32_t d, uint32_t a_tmem, uint64_t b,
                                                  uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -151,6 +148,20 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
       "r"(r[15])
       : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
+               : "memory");
+}
+
+// fp16 pair, a -> low half (RNE): the inverse chain's operands
+__device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
 }
 
 __device__ __forceinline__ void tmem_wait_st() {
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
   using G = Geo<BW>;
   constexpr int kEpiThreads = G::kEpiThreads;
   constexpr uint32_t kBandBytes = G::kBandBytes, kOffX = G::kOffX, kOffB7 = G::kOffB7;
-  constexpr uint32_t kB7Lo = G::kB7Lo, kOffOut = G::kOffOut, kOffC = G::kOffC;
+  constexpr uint32_t kOffOut = G::kOffOut, kOffC = G::kOffC;
   constexpr uint32_t kTD1 = G::kTD1, kTD2 = G::kTD2, kTD4 = G::kTD4;
   constexpr int kOut = G::kOutW;
   extern __shared__ uint8_t smem_raw[];
@@ -315,11 +326,12 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     // ------------------------------------------------------------ MMA issuer
     const uint32_t id128 = make_idesc(kFmtBF16, 128, BW, /*A K-major*/ 0, /*B MN*/ 1);
     const uint32_t id16 = make_idesc(kFmtBF16, 128, 16, 0, 0);
-    const uint32_t idtf = make_idesc(kFmtTF32, 128, 16, 0, 0);
+    const uint32_t id16h = make_idesc(kFmtF16, 128, 16, 0, 0);
+    const uint32_t id128h = make_idesc(kFmtF16, 128, BW, 0, 1);
     const uint64_t a_tmpl = make_sdesc(0u, 128u, 256u, kSwizzleNone);
     const uint32_t c4 = (base_s + kOffC) >> 4;
     const uint64_t b3 = make_sdesc(base_s + kOffC + kCB3, 128u, 256u, kSwizzleNone);
-    const uint64_t b5 = make_sdesc(base_s + kOffC + kCB5, 128u, 512u, kSwizzleNone);
+    const uint64_t b5 = make_sdesc(base_s + kOffC + kCB5, 128u, 256u, kSwizzleNone);
     const uint64_t b7 = make_sdesc(base_s + kOffB7, 16384u, 1024u, kSwizzle128B);
     mbar_wait(cbar, 0);
     // S1: D1 = T_p · X, 8 (p = 0) or 7 (p = 1) K-steps of 16 band rows, A
@@ -377,13 +389,9 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
           mbar_wait(&e2[q], ph);
           tc_fence_after();
 #pragma unroll
-          for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              mma_tf32_ts_elect(tmem + kTD1 + 16u * j + 8u * q,
-                                tmem + kTD2 + 16u * (G::kNq0 * q + j) + 8u * h,
-                                b5 + 16u * h, idtf, (q > 0 || h > 0) ? 1u : 0u);
-          }
+          for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j)
+            mma_f16_ts_elect(tmem + kTD1 + 16u * j + 8u * q, tmem + kTD2 + 16u * (G::kNq0 * q + j),
+                             b5, id16h, q > 0 ? 1u : 0u);
         }
         mma_commit_elect(s5done);
         // E3 has read D3: the next row phase's S1 (this band's p = 1, or the
@@ -403,14 +411,13 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
           }
         };
         next_s1();
-        // ---- S7: column inverse, D4 += T_pᵀ · B7 (hi + lo)
+        // ---- S7: column inverse, D4 += T_pᵀ · B7 (fp16)
         if (p == 0 && it > 0) mbar_wait(e4, (it - 1) & 1);  // previous band's E4 read D4
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < (p == 0 ? 8 : 7); ++k) {
           const uint64_t ad = a_tmpl | (c4 + kCS7 / 16 + (15u - 2u * k - p) * 16u);
-          mma_f16_ss_elect(tmem + kTD4, ad, b7 + 128u * k, id128, (p > 0 || k > 0) ? 1u : 0u);
-          mma_f16_ss_elect(tmem + kTD4, ad, b7 + 128u * k + kB7Lo / 16, id128, 1u);
+          mma_f16_ss_elect(tmem + kTD4, ad, b7 + 128u * k, id128h, (p > 0 || k > 0) ? 1u : 0u);
         }
         mma_commit_elect(s7done);
         ph ^= 1;
@@ -542,7 +549,11 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
                 v[c][l] = __float_as_uint(y);
               }
               if (dc_row) v[c][0] = dc;  // DC coefficient kept
-              tmem_st16(tl + kTD2 + 16u * ch, v[c]);
+              uint32_t h[8];  // fp16 pairs: the S5 A operand (K = 16 in 8 columns)
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                h[e] = pack_f16x2(__uint_as_float(v[c][2 * e]), __uint_as_float(v[c][2 * e + 1]));
+              tmem_st8(tl + kTD2 + 16u * ch, h);
             }
           }
           tmem_wait_st();
@@ -550,7 +561,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
           warp_arrive(&e2[q], lane);
         }
         if (et == 0) stamp(P, it, 12 * p + 3);
-        // ---- E3: D3 (lane f, BW columns) -> B7[f][c] hi/lo (MN-major, 128B swizzle)
+        // ---- E3: D3 (lane f, BW columns) -> B7[f][c] fp16 (MN-major, 128B swizzle)
         mbar_wait(s5done, ph);
         tc_fence_after();
         if (et == 0) stamp(P, it, 12 * p + 4);
@@ -563,14 +574,13 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
           tmem_wait_ld();
 #pragma unroll
           for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
-            uint32_t hi[4], lo[4];
+            uint32_t h[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              hi[e] = hi_lo(__uint_as_float(v[g >> 1][8 * (g & 1) + 2 * e]),
-                            __uint_as_float(v[g >> 1][8 * (g & 1) + 2 * e + 1]), &lo[e]);
-            const uint32_t off = sw_off(row, 32 * sp + 8 * g);
-            *reinterpret_cast<uint4*>(b7 + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<uint4*>(b7 + kB7Lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+              h[e] = pack_f16x2(__uint_as_float(v[g >> 1][8 * (g & 1) + 2 * e]),
+                                __uint_as_float(v[g >> 1][8 * (g & 1) + 2 * e + 1]));
+            *reinterpret_cast<uint4*>(b7 + sw_off(row, 32 * sp + 8 * g)) =
+                make_uint4(h[0], h[1], h[2], h[3]);
           }
         }
         tc_fence_before();
@@ -619,34 +629,49 @@ static void build_consts(uint8_t* out) {
     std::memcpy(&f, &b, 4);
     return static_cast<double>(f);
   };
+  // fp16 bits, round to nearest even (|v| < 1: normal or subnormal range)
+  auto f16_bits = [](double v) {
+    const float f = static_cast<float>(v);
+    uint32_t b;
+    std::memcpy(&b, &f, 4);
+    const uint32_t sign = (b >> 16) & 0x8000u;
+    const float a = std::fabs(f);
+    if (a < 6.103515625e-05f) {  // subnormal: units of 2^-24
+      return static_cast<uint16_t>(sign | static_cast<uint32_t>(std::nearbyint(a * 16777216.0f)));
+    }
+    uint32_t e = ((b >> 23) & 0xFFu) - 127u + 15u, m = b & 0x7FFFFFu;
+    uint32_t h = (e << 10) | (m >> 13);
+    const uint32_t rem = m & 0x1FFFu;
+    if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
+    return static_cast<uint16_t>(sign | h);
+  };
   // K-major no-swizzle core matrices, 16 K: element (row n, k) of a bf16 operand
   auto put16 = [&](uint8_t* dst, int n, int kk, double v, int lo) {
     uint16_t h = bf16_bits(v);
     if (lo) h = bf16_bits(v - bf16_val(h));
     std::memcpy(dst + (n / 8) * 256 + (kk / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2, &h, 2);
   };
-  // f32 K-major core matrices (8 n x 4 k): (n/8)*512 + (k/4)*128 + (n%8)*16 + (k%4)*4
-  auto put32 = [&](uint8_t* dst, int n, int kk, double v) {
-    const float f = static_cast<float>(v);
-    std::memcpy(dst + (n / 8) * 512 + (kk / 4) * 128 + (n % 8) * 16 + (kk % 4) * 4, &f, 4);
+  auto put16h = [&](uint8_t* dst, int n, int kk, double v) {
+    const uint16_t h = f16_bits(v);
+    std::memcpy(dst + (n / 8) * 256 + (kk / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2, &h, 2);
   };
   // S1 strip: row g, K = band row within the K-step.  Step k reads rows
   // g = f + 112 - 16k, so tile i = k sits at g in [112, 128).
   for (int lo = 0; lo < 2; ++lo)
     for (int k = 0; k < 16; ++k)
       for (int kk = 0; kk < 16; ++kk) put16(out + lo * dct::kStripBytes, 112 + k, kk, D[k][kk], lo);
-  // S7 strip: A7[r][kk] = Dw[kk][r - 16k - 8p] at g = r + 120 - 16k - 8p
+  // S7 strip (fp16): A7[r][kk] = Dw[kk][r - 16k - 8p] at g = r + 120 - 16k - 8p
   for (int m = 0; m < 16; ++m)
-    for (int kk = 0; kk < 16; ++kk) put16(out + dct::kCS7, 120 + m, kk, D[kk][m], 0);
+    for (int kk = 0; kk < 16; ++kk) put16h(out + dct::kCS7, 120 + m, kk, D[kk][m]);
   // B3[K = sample c][N = freq l] = Dw[l][c]: hi, lo
   for (int l = 0; l < 16; ++l)
     for (int c = 0; c < 16; ++c) {
       put16(out + dct::kCB3, l, c, D[l][c], 0);
       put16(out + dct::kCB3 + 512, l, c, D[l][c], 1);
     }
-  // B5[K = freq l][N = sample c] = Dw[l][c] (f32)
+  // B5[K = freq l][N = sample c] = Dw[l][c] (fp16)
   for (int c = 0; c < 16; ++c)
-    for (int l = 0; l < 16; ++l) put32(out + dct::kCB5, c, l, D[l][c]);
+    for (int l = 0; l < 16; ++l) put16h(out + dct::kCB5, c, l, D[l][c]);
 }
 
 template <int BW, typename OutT, bool SOFT>
