@@ -6,21 +6,23 @@
 // domain (hard or soft threshold; DC kept), clamp-to-edge outside the image.
 //
 // One persistent CTA per SM; work unit = a 128x128 input band at image
-// offset (Y-8, X-8) producing the 112x112 output block (Y.., X..).  The
-// 16x16 tiles of the band split into row phases p (tiles at band rows
-// 16i+8p) and column phases q (band columns 16j+8q).  Per row phase, with
-// f = 16i + k the (tile row, row frequency) index — the TMEM lane:
+// offset (Y-8, X-8) producing the 112x112 output block (Y.., X..).  The 15
+// tile rows of the band (tile row t starts at band row 8t) split into two
+// groups g (t = 8g .. 8g+7) that run the chain one after the other; column
+// phases q are tiles at band columns 16j+8q.  Per group, with
+// f = 16 (t - 8g) + k the (tile row, row frequency) index — the TMEM lane:
 //
-//   S1  (SS bf16, N=128)  D1[f][c]  = Σ_r T_p[f][r] X[r][c]
-//         A = T_p, the block-banded forward column transform (a shifted
-//         strip, hi + lo), B = the band straight from TMA (MN-major)
+//   S1  (SS bf16, N=128)  D1[f][c]  = Σ_r T_g[f][r] X[r][c]
+//         A = T_g, the banded forward column transform (windows of one
+//         constant strip, hi + lo; a 16-row K-step feeds 3 tile rows, so
+//         the band takes 9 K-steps), B = the band straight from TMA (MN-major)
 //   C1  D1 -> bf16 hi/lo pairs, in TMEM (no shared-memory round trip)
 //   S3  (TS bf16, N=16)   D2[f][16(8q+j)+l] = Σ_c D1[f][16j+8q+c] Dw[l][c]
 //         (hi·hi + lo·hi + hi·lo), A read from TMEM
 //   E2  coring of D2 (DC kept) -> fp16 pairs in place
 //   S5  (TS f16, N=16)    D3[f][16j+8q+c] (+)= Σ_l D2'[f][..+l] Dw[l][c]
 //   E3  D3 -> B7 (fp16, MN-major: K = f, N = c) in shared memory
-//   S7  (SS f16, N=128)   D4[r][c] += Σ_f T_pᵀ[r][f] B7[f][c]   (both p accumulate)
+//   S7  (SS f16, N=128)   D4[r][c] += Σ_f T_gᵀ[r][f] B7[f][c]   (both g accumulate)
 //   E4  D4 (lane = band row) -> output block, one TMA store
 //
 // Precision: the forward chain decides coring, so its f32 intermediates
@@ -59,11 +61,11 @@ void get_trace(unsigned long long** buf, int* ctas, int* tiles);
 namespace dct {
 
 // constants (built on the host, one bulk copy per CTA):
-//   S1 strip : hi, lo: 240 rows x 16 K, K-major core matrices (7680 B each)
+//   S1 strip : hi, lo: 256 rows x 16 K, K-major core matrices (8192 B each)
 //   S7 strip : 248 rows x 16 K
 //   B3       : Dwᵀ as the S3 B operand (K = sample, N = freq), hi + lo
 //   B5       : Dw f32 (K = freq, N = sample) for S5
-constexpr uint32_t kStripBytes = 7680;
+constexpr uint32_t kStripBytes = 8192;
 constexpr uint32_t kCS7 = 2 * kStripBytes;
 constexpr uint32_t kCB3 = kCS7 + 7936;
 constexpr uint32_t kCB5 = kCB3 + 1024;
@@ -92,12 +94,16 @@ struct Geo {
   static constexpr uint32_t kOffC = kOffOut + round1k(kOutRows * kOutW * 4);
   static constexpr uint32_t kOffBar = kOffC + kConstBytes;
   static constexpr uint32_t kSmem = kOffBar + 256 + 1024;
-  // TMEM columns: D1 f32 / packed pairs (hi [0, BW/2), lo [BW/2, BW)) / D3;
-  // D2 (kChunks x 16); D4 (BW)
-  static constexpr uint32_t kTD1 = 0, kTD2 = BW, kTD4 = BW + 16 * kChunks;
+  // TMEM columns: D1 f32 / packed pairs (hi [0, BW/2), lo [BW/2, BW));
+  // D2 region [BW, 3 BW): S3's f32 chunks (kChunks x 16), cored into fp16
+  // pairs packed at kTD2 + 8 ch, and D3 in the region's upper half (over the
+  // q = 1 f32 chunks, consumed by then); D4 (BW).  D1 is not reused, so the
+  // next row phase's S1 runs while this one is cored and inverted.
+  static constexpr uint32_t kTD1 = 0, kTD2 = BW, kTD3 = 2 * BW, kTD4 = 3 * BW;
   static constexpr int kTmemCols = BW == 128 ? 512 : 256;
   static constexpr int kMinBlocks = BW == 128 ? 1 : 2;
   static_assert(kTD4 + BW <= static_cast<uint32_t>(kTmemCols), "TMEM budget");
+  static_assert(16 * kChunks <= 2 * BW && 8 * kChunks <= BW, "D2 region");
 };
 
 struct Params {
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
   constexpr int kEpiThreads = G::kEpiThreads;
   constexpr uint32_t kBandBytes = G::kBandBytes, kOffX = G::kOffX, kOffB7 = G::kOffB7;
   constexpr uint32_t kOffOut = G::kOffOut, kOffC = G::kOffC;
-  constexpr uint32_t kTD1 = G::kTD1, kTD2 = G::kTD2, kTD4 = G::kTD4;
+  constexpr uint32_t kTD1 = G::kTD1, kTD2 = G::kTD2, kTD3 = G::kTD3, kTD4 = G::kTD4;
   constexpr int kOut = G::kOutW;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_s = smem_u32(smem_raw);
@@ -334,24 +340,24 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     const uint64_t b5 = make_sdesc(base_s + kOffC + kCB5, 128u, 256u, kSwizzleNone);
     const uint64_t b7 = make_sdesc(base_s + kOffB7, 16384u, 1024u, kSwizzle128B);
     mbar_wait(cbar, 0);
-    // S1: D1 = T_p · X, 8 (p = 0) or 7 (p = 1) K-steps of 16 band rows, A
-    // strip hi + lo.  Row phase 1 reuses the phase-0 strip with the band
-    // descriptor moved down 8 rows (one 1 KB swizzle atom): its tiles then
-    // start on K-step boundaries.
-    auto issue_s1 = [&](int s, int p) {
-      const uint64_t bx =
-          make_sdesc(base_s + kOffX + s * kBandBytes + p * 1024u, 16384u, 1024u, kSwizzle128B);
+    // S1: D1 = T_g · X for tile group g (tiles t = 8g .. 8g + 7, starting at
+    // band row 8t; lane 16 (t - 8g) + k).  K-step m (band rows 16m ..) feeds
+    // tiles 2m - 1, 2m, 2m + 1, so group 0 needs K-steps 0..4 and group 1
+    // K-steps 4..7: 9 K-steps x (hi, lo) per band.  A = a window of one
+    // constant strip, moved 32 lanes per K-step.
+    auto issue_s1 = [&](int s, int g) {
+      const uint64_t bx = make_sdesc(base_s + kOffX + s * kBandBytes, 16384u, 1024u, kSwizzle128B);
       tc_fence_after();
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (p == 1 && k == 7) break;
-        const uint32_t so = (14u - 2u * k) * 16u;  // strip offset, 16-byte units
-        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + so), bx + 128u * k, id128, k > 0 ? 1u : 0u);
-        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + kStripBytes / 16 + so), bx + 128u * k, id128,
+      for (int m = 4 * g; m < 5 + 3 * g; ++m) {
+        const uint32_t so = 256u - 64u * m + 256u * g;  // strip window, 16-byte units
+        const uint32_t acc = m > 4 * g ? 1u : 0u;
+        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + so), bx + 128u * m, id128, acc);
+        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + kStripBytes / 16 + so), bx + 128u * m, id128,
                          1u);
       }
       mma_commit_elect(s1done);  // before any later S7: C1 must not wait for it
-      if (p == 1) mma_commit_elect(&xempty[s]);
+      if (g == 1) mma_commit_elect(&xempty[s]);
     };
     int it = 0;
     uint32_t ph = 0;  // phase of the per-row-phase barriers (two completions per band)
@@ -380,43 +386,37 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
           }
           mma_commit_elect(&s3done[q]);  // E2 cores column phase q while S3 runs q + 1
         }
-        // ---- S5: row inverse (TS tf32, A = cored D2) into D3 (over D1): column
-        // phase q starts as soon as its coefficients are cored; D3 overwrites
-        // the packed D1, so every S3 MMA must have completed (s3done[1])
-        mbar_wait(&s3done[1], ph);
+        // The next row phase's S1 (this band's p = 1, or the next band's p = 0)
+        // goes right behind S3: D1 is free once S3 has read it (in-order
+        // tensor pipe), so its C1 can follow this phase's E3 without a wait.
+        if (p == 0) {
+          issue_s1(s, 1);
+        } else if (t + static_cast<int>(gridDim.x) < P.nregions) {
+          const int s2 = (it + 1) & 1;
+          mbar_wait(&xfull[s2], ((it + 1) >> 1) & 1);
+          mbar_wait(&xready[s2], ((it + 1) >> 1) & 1);
+          if (lane == 0) stamp(P, it + 1, 7);
+          issue_s1(s2, 0);
+        }
+        // ---- S5: row inverse (TS f16, A = cored D2 packed at kTD2 + 8 ch) into
+        // D3, which overlays the q = 1 f32 chunks: after all of E2
+        mbar_wait(&e2[1], ph);
+        tc_fence_after();
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          mbar_wait(&e2[q], ph);
-          tc_fence_after();
 #pragma unroll
           for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j)
-            mma_f16_ts_elect(tmem + kTD1 + 16u * j + 8u * q, tmem + kTD2 + 16u * (G::kNq0 * q + j),
+            mma_f16_ts_elect(tmem + kTD3 + 16u * j + 8u * q, tmem + kTD2 + 8u * (G::kNq0 * q + j),
                              b5, id16h, q > 0 ? 1u : 0u);
         }
         mma_commit_elect(s5done);
-        // E3 has read D3: the next row phase's S1 (this band's p = 1, or the
-        // next band's p = 0) goes first, so its C1 overlaps this phase's S7
-        // (measured neutral: the in-order tensor pipe then runs S7 ahead of
-        // the next S3 — kept for the shorter C1 wait)
         mbar_wait(e3, ph);
-        auto next_s1 = [&]() {
-          if (p == 0) {
-            issue_s1(s, 1);
-          } else if (t + static_cast<int>(gridDim.x) < P.nregions) {
-            const int s2 = (it + 1) & 1;
-            mbar_wait(&xfull[s2], ((it + 1) >> 1) & 1);
-            mbar_wait(&xready[s2], ((it + 1) >> 1) & 1);
-            if (lane == 0) stamp(P, it + 1, 7);
-            issue_s1(s2, 0);
-          }
-        };
-        next_s1();
         // ---- S7: column inverse, D4 += T_pᵀ · B7 (fp16)
         if (p == 0 && it > 0) mbar_wait(e4, (it - 1) & 1);  // previous band's E4 read D4
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < (p == 0 ? 8 : 7); ++k) {
-          const uint64_t ad = a_tmpl | (c4 + kCS7 / 16 + (15u - 2u * k - p) * 16u);
+        for (int k = 0; k < (p == 0 ? 8 : 7); ++k) {  // tile t = 8p + k
+          const uint64_t ad = a_tmpl | (c4 + kCS7 / 16 + (15u - 8u * p - k) * 16u);
           mma_f16_ss_elect(tmem + kTD4, ad, b7 + 128u * k, id128h, (p > 0 || k > 0) ? 1u : 0u);
         }
         mma_commit_elect(s7done);
@@ -519,13 +519,13 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         // ---- E2: coring of D2 (lane f, columns 16*(kNq0*q+j) + l) in place,
         // one column phase at a time
         const bool dc_row = (row & 15) == 0;
-        const float thr = P.threshold;
+        const float thr = P.threshold, nthr_big = -thr * 0x1p100f;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           mbar_wait(&s3done[q], ph);
           tc_fence_after();
           if (et == 0) stamp(P, it, 12 * p + (q == 0 ? 2 : 6));
-          if (sp == 0 && q == 1) dbg_dump(P, it, 1, p, tl + kTD2, row, 16 * G::kChunks);
+          if (sp == 0 && q == 0) dbg_dump(P, it, 1, p, tl + kTD2, row, 16 * G::kNq0);
           const int ch0 = q == 0 ? 0 : G::kNq0, ch1 = q == 0 ? G::kNq0 : G::kChunks;
           uint32_t v[2][16];
 #pragma unroll
@@ -533,6 +533,8 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
             if (ch0 + sp + G::kSplits * c < ch1)
               tmem_ld16(tl + kTD2 + 16u * (ch0 + sp + G::kSplits * c), v[c]);
           tmem_wait_ld();
+          // the packed q = 0 pairs overwrite f32 chunks other warps still read
+          if (q == 0) named_bar_sync(1, kEpiThreads);
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int ch = ch0 + sp + G::kSplits * c;
@@ -542,10 +544,16 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
               for (int l = 0; l < 16; ++l) {
                 const float x = __uint_as_float(v[c][l]);
                 float y;
-                if constexpr (SOFT)
-                  y = copysignf(fmaxf(fabsf(x) - thr, 0.0f), x);
-                else
-                  y = fabsf(x) < thr ? 0.0f : x;
+                // coring on the FMA pipe (the ALU pipe, 64 lanes/clk, also
+                // runs the fp16 packing): keep = sat((|x| - thr) * 2^100) is 1
+                // for |x| > thr and 0 below it (a compare + select would be
+                // two ALU instructions per coefficient)
+                if constexpr (SOFT) {
+                  const float d = fabsf(x) - thr;
+                  y = copysignf(d * __saturatef(d * 0x1p100f), x);
+                } else {
+                  y = x * __saturatef(fmaf(fabsf(x), 0x1p100f, nthr_big));
+                }
                 v[c][l] = __float_as_uint(y);
               }
               if (dc_row) v[c][0] = dc;  // DC coefficient kept
@@ -553,7 +561,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
 #pragma unroll
               for (int e = 0; e < 8; ++e)
                 h[e] = pack_f16x2(__uint_as_float(v[c][2 * e]), __uint_as_float(v[c][2 * e + 1]));
-              tmem_st8(tl + kTD2 + 16u * ch, h);
+              tmem_st8(tl + kTD2 + 8u * ch, h);
             }
           }
           tmem_wait_st();
@@ -565,12 +573,12 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         mbar_wait(s5done, ph);
         tc_fence_after();
         if (et == 0) stamp(P, it, 12 * p + 4);
-        if (sp == 0) dbg_dump(P, it, 2, p, tl + kTD1, row, BW);
+        if (sp == 0) dbg_dump(P, it, 2, p, tl + kTD3, row, BW);
         {
           uint8_t* b7 = base + kOffB7;
           uint32_t v[2][16];
-          tmem_ld16(tl + kTD1 + 32u * sp, v[0]);
-          tmem_ld16(tl + kTD1 + 32u * sp + 16u, v[1]);
+          tmem_ld16(tl + kTD3 + 32u * sp, v[0]);
+          tmem_ld16(tl + kTD3 + 32u * sp + 16u, v[1]);
           tmem_wait_ld();
 #pragma unroll
           for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
@@ -655,11 +663,17 @@ static void build_consts(uint8_t* out) {
     const uint16_t h = f16_bits(v);
     std::memcpy(dst + (n / 8) * 256 + (kk / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2, &h, 2);
   };
-  // S1 strip: row g, K = band row within the K-step.  Step k reads rows
-  // g = f + 112 - 16k, so tile i = k sits at g in [112, 128).
+  // S1 strip: the 48-row block of K-step m at strip rows 112 + 16 d + k
+  // (d = t - 2m + 1, tile t's frequency k; K = band row 16m + kk, i.e. tile
+  // row kk + 8 - 8d); K-step m of group g reads the window starting at
+  // strip row 128 - 32 m + 128 g, so that tile t lands on lane 16 (t - 8g) + k.
   for (int lo = 0; lo < 2; ++lo)
-    for (int k = 0; k < 16; ++k)
-      for (int kk = 0; kk < 16; ++kk) put16(out + lo * dct::kStripBytes, 112 + k, kk, D[k][kk], lo);
+    for (int d = 0; d < 3; ++d)
+      for (int k = 0; k < 16; ++k)
+        for (int kk = 0; kk < 16; ++kk) {
+          const int r = kk + 8 - 8 * d;
+          if (r >= 0 && r < 16) put16(out + lo * dct::kStripBytes, 112 + 16 * d + k, kk, D[k][r], lo);
+        }
   // S7 strip (fp16): A7[r][kk] = Dw[kk][r - 16k - 8p] at g = r + 120 - 16k - 8p
   for (int m = 0; m < 16; ++m)
     for (int kk = 0; kk < 16; ++kk) put16h(out + dct::kCS7, 120 + m, kk, D[kk][m]);
