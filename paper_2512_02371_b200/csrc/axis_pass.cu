@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kThreads)
     else
       tma_store_3d(&tm_out, stg, 16 * b0, 128 * strip, p);
     bulk_commit();
-    bulk_wait0();
+    bulk_wait_read0();  // smem may be released once read; the write completes on its own
   }
   if (warp == 1) {
     tc_fence_after();

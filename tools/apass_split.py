@@ -1,3 +1,5 @@
+import os as _os, sys as _sys
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import os, sys, torch
 from paper_2512_02371_b200 import pipelines
 shape, oh, ow = (48, 2160, 3840), 540, 960
