@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(128, 1) k(long long* out) {
   const uint32_t tmem = *slot;
   if (warp == 0) {
     const uint32_t idesc = make_idesc(kFmtBF16, 128, N, MODE == 2 ? 1u : 0u, MODE == 0 ? 1u : 0u);
+    (void)0;
     const uint64_t a0 = MODE == 2 ? make_sdesc(base_s, 16384u, 1024u, kSwizzle128B)
                                   : make_sdesc(base_s, 128u, 256u, kSwizzleNone);
     const uint64_t b0 = MODE == 0 ? make_sdesc(base_s + 65536u, 16384u, 1024u, kSwizzle128B)
@@ -56,7 +57,14 @@ __global__ void __launch_bounds__(128, 1) k(long long* out) {
       const uint32_t d = tmem + (MODE == 1 ? 256u : 0u) + (N <= 128 ? (i & 1) * N : 0u);
       if (MODE == 1)
         mma_ts(d, tmem + 8u * q, b0 + q * 32u, idesc, i > 1 ? 1u : 0u);
-      else
+      else if (MODE == 4) {  // S5 pattern: 8 tiles at 16j (overwrite), 7 at 16j + 8 (accumulate)
+        const int r = i % 16;
+        const uint32_t dd = r < 8 ? 256u + 16u * r : 256u + 16u * (r - 8) + 8u;
+        if (r < 15) mma_ts(tmem + dd, tmem + 8u * q, b0 + q * 32u, idesc, r >= 8 ? 1u : 0u);
+      } else if (MODE == 5) {  // same accumulator every MMA
+        mma_ts(tmem + 256u, tmem + 8u * q, b0 + q * 32u, idesc, i > 0 ? 1u : 0u);
+      }
+      else if (MODE != 4 && MODE != 5)
         mma_f16_ss_elect(d, a0 + q * (MODE == 2 ? 128u : 256u), b0 + q * (MODE == 0 ? 128u : 32u), idesc,
                          i > 1 ? 1u : 0u);
     }
@@ -101,5 +109,7 @@ int main() {
   run<2, 32>("SS A MNmaj-SW128, B Kmaj-noswz");
   run<3, 16>("SS A Kmaj-noswz, B Kmaj-noswz");
   run<3, 128>("SS A Kmaj-noswz, B Kmaj-noswz");
+  run<4, 16>("TS S5 pattern (x60/64 issued)");
+  run<5, 16>("TS one accumulator chain");
   return 0;
 }
