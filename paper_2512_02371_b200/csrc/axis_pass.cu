@@ -16,7 +16,8 @@
 // each block's K window streams through an 8-slot TMA ring with no upper
 // bound on its length (windows up to 1024 inputs, i.e. ~45x downscale), the
 // blocks accumulate into adjacent 16-column TMEM slices and leave in one TMA
-// store.  Two CTAs share an SM (<= ~104 KB smem, 128 TMEM columns each).
+// store.  Several CTAs share an SM (the ring depth, group size and TMEM
+// columns are sized per pass so that loads from many CTAs overlap).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -50,6 +51,8 @@ struct Params {
   int planes, nb, nstrip;  // blocks along the axis, 128-wide strips across it
   int nbg, ngroups;        // blocks per CTA (<= 8) and block groups
   int nunits;
+  uint32_t tmem_cols;  // accumulator columns: 16 per block, power of two >= 32
+  int nring;  // ring slots in use (<= Ring::kSlots): a group never needs more than it loads
   uint32_t off_b, off_out, off_bar;
 };
 
@@ -64,7 +67,8 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t tile_bytes = static_cast<uint32_t>(P.ax.tile_bytes);
   // [ring][B tiles of the group][staging][barriers]
   using RG = Ring<VERT>;
-  constexpr int kRing = RG::kSlots;
+  constexpr int kRing = RG::kSlots;  // barrier array size
+  const int nring = P.nring;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + P.off_bar);
   uint64_t* full = bars;
   uint64_t* empty = bars + kRing;
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(kThreads)
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<128>(tmem_slot);
+  if (warp == 1) tmem_alloc_n(tmem_slot, P.tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(kThreads)
           } else {     // rows 128*strip.., columns ws+64q.. as one 64-column box
             tma_load_3d(dst, &tm_in, &full[s], ws + 64 * q, 128 * strip, p);
           }
-          if (++s == kRing) {
+          if (++s == nring) {
             s = 0;
             ph ^= 1;
           }
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(kThreads)
                              idesc, q > 0 ? 1u : 0u);
         }
         mma_commit_elect(&empty[s]);
-        if (++s == kRing) {
+        if (++s == nring) {
           s = 0;
           ph ^= 1;
         }
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<128>(tmem);
+    tmem_dealloc_n(tmem, P.tmem_cols);
   }
 }
 
@@ -261,18 +265,35 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   const uint32_t tb = static_cast<uint32_t>(a->tile_bytes);
   const int64_t base_units = static_cast<int64_t>(planes) * a->nb * P.nstrip;
   P.nbg = 1;
-  // (thresholds measured on B200: 4K->540p and 2048^2->{143,450,921}^2)
-  const int64_t want = dim == 0 ? 148 * 64 : 148 * 24;
-  while (P.nbg < 8 && base_units / (2 * P.nbg) >= want && (2u * P.nbg) * tb <= 32768u)
-    P.nbg *= 2;
+  // (measured on B200, tools/sweep_apass.sh: 4K->540p and 2048^2->{143,450,921}^2)
+  if (dim == 0) {
+    const int64_t want = 148 * 64;
+    if (base_units / 2 >= want && 2u * tb <= 32768u) P.nbg = 2;
+  } else if (base_units >= 148 * 32 && 2u * tb <= 32768u) {
+    P.nbg = 2;  // horizontal: small CTAs, many per SM
+  }
   if (const char* f = std::getenv("TSB_APASS_NBG")) P.nbg = std::atoi(f) > 0 ? std::atoi(f) : 1;
   if (P.nbg > P.nb) P.nbg = P.nb;
   P.ngroups = (P.nb + P.nbg - 1) / P.nbg;
+  P.tmem_cols = 32;
+  while (P.tmem_cols < 16u * P.nbg) P.tmem_cols *= 2;
   const int64_t units = static_cast<int64_t>(planes) * P.ngroups * P.nstrip;
   if (units > 0x7FFFFFFF) return set_error(TS_ERR_UNSUPPORTED, "axis_pass: too many blocks");
   P.nunits = static_cast<int>(units);
-  P.off_b = dim == 0 ? apass::Ring<true>::kSlots * apass::Ring<true>::kSlot
-                     : apass::Ring<false>::kSlots * apass::Ring<false>::kSlot;
+  {
+    const int kslots = dim == 0 ? apass::Ring<true>::kSlots : apass::Ring<false>::kSlots;
+    const int ksteps = dim == 0 ? apass::Ring<true>::kSteps : apass::Ring<false>::kSteps;
+    const int per_block = (a->K / 16 + ksteps - 1) / ksteps;
+    // vertical: 4 of the 6 slots; horizontal: one 64-column slot (the
+    // short-lived CTAs then fit ~7 per SM, which keeps more loads in flight
+    // than a deeper ring per CTA)
+    P.nring = dim == 0 ? 4 : 1;
+    if (const char* f = std::getenv("TSB_APASS_RING")) P.nring = std::atoi(f);
+    if (P.nring > P.nbg * per_block) P.nring = P.nbg * per_block;
+    if (P.nring < 1) P.nring = 1;
+    if (P.nring > kslots) P.nring = kslots;
+  }
+  P.off_b = P.nring * (dim == 0 ? apass::Ring<true>::kSlot : apass::Ring<false>::kSlot);
   P.off_out = P.off_b + ((static_cast<uint32_t>(P.nbg) * tb + 1023u) & ~1023u);
   P.off_bar = P.off_out + ((128u * 16u * P.nbg * oes + 1023u) & ~1023u);
   const uint32_t smem = P.off_bar + 256u + 1024u;
