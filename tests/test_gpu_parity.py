@@ -221,3 +221,30 @@ def test_upsample_3x_and_non_integer(shape, oh, ow):
     y = _gpu(pipelines.resample, x, out_h=oh, out_w=ow, out_dtype=torch.float32)
     ref = pipelines_ref.resample(x, oh, ow)
     assert np.abs(y - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("nbg,ring", [("1", "1"), ("2", "1"), ("2", "4"), ("4", "3"), ("8", "6")])
+def test_axis_pass_tuning_knobs_do_not_change_results(nbg, ring):
+    """The axis pass's group size (blocks per CTA) and TMA ring depth are
+    performance knobs only: every setting gives bit-identical output (the
+    per-block K accumulation order does not depend on them)."""
+    import subprocess, sys, os
+    code = (
+        "import torch, numpy as np, sys\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_2512_02371_b200 import pipelines\n"
+        "g = torch.Generator().manual_seed(7)\n"
+        "x = torch.rand((2, 2048, 640), generator=g).bfloat16().cuda()\n"
+        "from paper_2512_02371_b200 import axis\n"
+        "assert not pipelines.fused_supported(axis.lanczos3(2048, 143, 0), axis.lanczos3(640, 100, 0))\n"
+        "y = pipelines.resample(x, 143, 100).float().cpu().numpy()\n"
+        "np.save(sys.argv[1], y)\n") % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"TSB_APASS_NBG": nbg, "TSB_APASS_RING": ring}):
+        import tempfile
+        f = tempfile.NamedTemporaryFile(suffix=".npy", delete=False).name
+        subprocess.run([sys.executable, "-c", code, f], check=True, env={**os.environ, **env},
+                       timeout=300)
+        outs.append(np.load(f))
+        os.unlink(f)
+    assert np.array_equal(outs[0], outs[1])
