@@ -4,6 +4,14 @@ GPU executor: the program (reference .sexp syntax) runs through
 `executor.run_program`, inputs come from a buffer directory (interp.py:640-678)
 or the seeded fills, results can be written back as a buffer directory.
 
+`python -m paper_2512_02371_b200 difftest FILE [--trials N] [--seed S] [--ulp U]
+[--json]` is the reference's `difftest` (cli.py:131-183) with the two sides
+being the GPU executor and the reference interpreter itself
+(`tensorsel.interp.run_program`, imported from the environment or from the
+offline install under baseline/_ref): every output parameter compared
+bitwise (or within --ulp) over `trials` seeded fills; the report has the
+reference's DiffTestResult fields.
+
 Exit codes as the reference's (cli.py:3-6): 0 success, 1 evaluation failure
 (EvalError: OutOfBounds, ShapeUnregistered, ... or UnsupportedProgram for
 statements outside the convolution family), 2 usage or parse failure.  The
@@ -75,6 +83,86 @@ def cmd_run(args) -> int:
     return 0
 
 
+def _reference_interp():
+    """The reference package (tensorsel) — only the difftest uses it."""
+    try:
+        import tensorsel  # noqa: F401
+    except ImportError:
+        ref = Path(__file__).resolve().parent.parent / "baseline" / "_ref"
+        if ref.is_dir():
+            sys.path.insert(0, str(ref))
+    try:
+        from tensorsel import interp as rinterp, ir as rir
+    except ImportError:
+        return None
+    return rinterp, rir
+
+
+def _ulp_equal(a, b, ulps) -> bool:
+    """The reference's comparison (cli.py:121-128): bitwise, or within `ulps`
+    units in the last place of the f32 carriers (ints exactly)."""
+    import numpy as np
+    if a.dtype == np.int64 or b.dtype == np.int64:
+        return np.array_equal(a, b)
+    ai = np.asarray(a, np.float32).view(np.int32).astype(np.int64)
+    bi = np.asarray(b, np.float32).view(np.int32).astype(np.int64)
+    ai = np.where(ai < 0, -(2**31) - ai, ai)
+    bi = np.where(bi < 0, -(2**31) - bi, bi)
+    return bool(np.all(np.abs(ai - bi) <= ulps))
+
+
+def cmd_difftest(args) -> int:
+    import numpy as np
+    from . import executor, fills
+    from .errors import EvalError
+    prog = _load(args.file)
+    ref = _reference_interp()
+    if ref is None:
+        print("error: the reference interpreter (tensorsel) is not importable; install it "
+              "offline under baseline/_ref", file=sys.stderr)
+        return 2
+    rinterp, rir = ref
+    try:
+        rprog = rir.parse_program(Path(args.file).read_text())
+    except Exception as e:  # the reference's own parse error
+        print(f"error: {args.file}: {e}", file=sys.stderr)
+        return 2
+    result = {"program": Path(args.file).stem, "trials": args.trials, "seeds": [],
+              "selection_ok": True, "divergence": None}
+    try:
+        for t in range(args.trials):
+            seed = args.seed + t
+            result["seeds"].append(seed)
+            inputs = fills.random_inputs(prog, seed)
+            out_gpu = executor.run_program(prog, inputs)
+            out_ref = rinterp.run_program(rprog, {k: np.array(v) for k, v in inputs.items()})
+            for prm in prog.params:
+                a = np.asarray(out_ref[prm.name].data)
+                b = np.asarray(out_gpu[prm.name].data)
+                same = (_ulp_equal(a, b, args.ulp) if args.ulp
+                        else a.astype(b.dtype).tobytes() == b.tobytes())
+                if not same:
+                    lane = int(np.nonzero(a != b)[0][0])
+                    result["divergence"] = {"seed": seed, "buffer": prm.name, "lane": lane,
+                                            "lhs": float(a[lane]), "rhs": float(b[lane])}
+                    break
+            if result["divergence"]:
+                break
+    except EvalError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+    if args.json:
+        print(json.dumps(result, indent=2))
+    else:
+        status = "diverged" if result["divergence"] else "ok"
+        print(f"{result['program']}: {len(result['seeds'])} trials: {status}")
+        if result["divergence"]:
+            d = result["divergence"]
+            print(f"  seed {d['seed']} buffer {d['buffer']} lane {d['lane']}: "
+                  f"{d['lhs']} vs {d['rhs']}")
+    return 1 if result["divergence"] else 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2512_02371_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -85,11 +173,20 @@ def main(argv=None) -> int:
     g.add_argument("--inputs", help="directory with manifest.json and .bin buffers")
     p.add_argument("--output", help="write the final buffers to this directory")
     p.add_argument("--json", action="store_true", help="JSON output")
+    p.set_defaults(fn=cmd_run)
+    p = sub.add_parser("difftest", help="GPU executor vs the reference interpreter, "
+                                        "bitwise or within --ulp, over seeded fills")
+    p.add_argument("file")
+    p.add_argument("--trials", type=int, default=100)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--ulp", type=int, default=0, help="tolerate this many ULPs (default: bitwise)")
+    p.add_argument("--json", action="store_true", help="JSON output")
+    p.set_defaults(fn=cmd_difftest)
     try:
         args = ap.parse_args(argv)
     except SystemExit as e:
         return 2 if e.code else 0
     try:
-        return cmd_run(args)
+        return args.fn(args)
     except SystemExit as e:
         return int(e.code)

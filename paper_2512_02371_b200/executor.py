@@ -100,6 +100,11 @@ def _eval_index(e, env):
     raise UnsupportedProgram(f"index expression {c}")
 
 
+def _unit_ramp(index):
+    return (_cls(index) == "Ramp" and _cls(index.stride) == "Imm"
+            and int(index.stride.value) == 1)
+
+
 def _is_flat(index, length=None):
     return (_cls(index) == "Ramp" and _cls(index.base) == "Imm" and int(index.base.value) == 0
             and _cls(index.stride) == "Imm" and int(index.stride.value) == 1
@@ -248,7 +253,14 @@ def _compile(p, extra_shapes, strict):
                 return
         # dst = Load src (flat copy)
         if vc == "Load" and _is_flat(s.index) and _is_flat(v.index, s.index.steps):
-            plan.ops.append(("copy", s.buffer, v.buffer, s.index.steps))
+            plan.ops.append(("copy", s.buffer, v.buffer, s.index.steps, 0, 0))
+            return
+        # dst[ramp(bd, 1, n)] = Load src[ramp(bs, 1, n)]: a window copy at affine
+        # offsets (e.g. each For iteration's accumulator into its output slot)
+        if vc == "Load" and _unit_ramp(s.index) and _unit_ramp(v.index) \
+                and v.index.steps == s.index.steps:
+            plan.ops.append(("copy", s.buffer, v.buffer, s.index.steps,
+                             _eval_int(s.index.base, env), _eval_int(v.index.base, env)))
             return
         if vc == "Broadcast" and _cls(v.operand) == "Imm" and _is_flat(s.index):
             plan.ops.append(("fill", s.buffer, float(v.operand.value), s.index.steps))
@@ -364,8 +376,11 @@ def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=N
             _, name, val, n = op
             bufs[name][:, :n] = val
         elif kind == "copy":
-            _, dst, src, n = op
-            bufs[dst][:, :n] = bufs[src][:, :n]
+            _, dst, src, n, bd, bs = op
+            for name, b in ((dst, bd), (src, bs)):
+                if b < 0 or b + n > bufs[name].shape[1]:
+                    raise OutOfBounds(name, b if b < 0 else b + n - 1)
+            bufs[dst][:, bd:bd + n] = bufs[src][:, bs:bs + n]
         elif kind == "tmp":
             _, name, kbuf, base, off = op
             K = bufs[kbuf]

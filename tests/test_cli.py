@@ -73,3 +73,56 @@ def test_cli_run_matches_reference_outputs(golden, G, name, tmp_path):
     out2 = tmp_path / "out2"
     assert cli.main(["run", str(src), "--inputs", str(out), "--output", str(out2)]) == 0
     assert (out2 / "manifest.json").exists()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["conv1d_k8", "conv1d_k16", "conv2d_outer_ry",
+                                  "downsample2_1d", "upsample2_1d"])
+@pytest.mark.parametrize("form", ["source", "lowered"])
+def test_cli_difftest_gpu_vs_reference_interpreter(golden, name, form, tmp_path):
+    """`difftest` (the reference's cli.py:131-183, with the GPU executor and
+    the reference interpreter as the two sides): bitwise over seeded fills."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "tensorsel")):
+        pytest.skip("reference interpreter not installed under baseline/_ref")
+    src = tmp_path / f"{name}.sexp"
+    src.write_text(golden["programs"][name][form])
+    r = subprocess.run([sys.executable, "-m", "paper_2512_02371_b200", "difftest", str(src),
+                        "--trials", "8", "--seed", "3", "--json"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rep = json.loads(r.stdout)
+    assert rep["divergence"] is None and rep["seeds"] == list(range(3, 11))
+
+
+def _lanczos_stream_program(n):
+    """An image-scale generated program: the Lanczos-3 2x conv statement
+    (12 taps, stride 2; the golden `lanczos_tile` statement) inside a For loop
+    over `n` consecutive 256-output windows of one long row."""
+    body = ("(store conv (ramp (imm i32 0) (imm i32 1) 256) (broadcast (imm f32 0.0) 256)) "
+            "(store conv (ramp (imm i32 0) (imm i32 1) 256) (add (vector-reduce-add 256 "
+            "(mul (cast (f32 3072) (load I (f16 3072) (ramp (ramp (mul (imm i32 512) (var t)) "
+            "(imm i32 1) 12) (broadcast (imm i32 2) 12) 256))) (broadcast (cast (f32 12) "
+            "(load K (f16 12) (ramp (imm i32 0) (imm i32 1) 12))) 256))) (load conv (f32 256) "
+            "(ramp (imm i32 0) (imm i32 1) 256)))) "
+            "(store output (ramp (mul (imm i32 256) (var t)) (imm i32 1) 256) "
+            "(load conv (f32 256) (ramp (imm i32 0) (imm i32 1) 256)))")
+    return (f"(param K f16 12 mem)\n(param I f16 {512 * n + 12} mem)\n"
+            f"(param output f32 {256 * n} mem)\n(wmma-shape 32 28 8)\n"
+            f"(allocate conv f32 256 wmma)\n(for t 0 {n} {body})\n")
+
+
+@pytest.mark.gpu
+def test_cli_difftest_image_scale_generated_program(tmp_path):
+    """SURVEY §8(f)1's gate at image scale: 512 Lanczos windows (131072
+    outputs) per trial, GPU executor vs the reference interpreter, bitwise."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "tensorsel")):
+        pytest.skip("reference interpreter not installed under baseline/_ref")
+    src = tmp_path / "lanczos_stream.sexp"
+    src.write_text(_lanczos_stream_program(512))
+    r = subprocess.run([sys.executable, "-m", "paper_2512_02371_b200", "difftest", str(src),
+                        "--trials", "2", "--json"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert json.loads(r.stdout)["divergence"] is None
