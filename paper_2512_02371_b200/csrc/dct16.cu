@@ -775,14 +775,15 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
       d_consts[dev] = d;
     }
   }
-  // band width: 128 columns (one CTA per SM) unless TSB_DCT_BAND=64 (two
-  // CTAs per SM; within 1% since E4 moved off the critical path)
+  // band width: 64 columns, two CTAs (two independent chains) per SM, unless
+  // TSB_DCT_BAND=128 (one CTA per SM): 2% faster on B200 (82 vs 84 us per
+  // 4K frame, same-box A/B, tools/ab_env.sh)
   const char* v = std::getenv("TSB_DCT_BAND");
-  if (v && std::atoi(v) == 64)
-    return dct16_run_bw<64>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
-                            threshold, soft, d_consts[dev], stream);
-  return dct16_run_bw<128>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
-                           threshold, soft, d_consts[dev], stream);
+  if (v && std::atoi(v) == 128)
+    return dct16_run_bw<128>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
+                             threshold, soft, d_consts[dev], stream);
+  return dct16_run_bw<64>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
+                          threshold, soft, d_consts[dev], stream);
 }
 
 }  // namespace tsb

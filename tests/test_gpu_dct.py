@@ -69,10 +69,10 @@ def test_denoising_reduces_error():
 
 
 @pytest.mark.parametrize("shape", [(1, 136, 248), (2, 232, 360)])
-def test_half_band_variant_matches_oracle(shape, monkeypatch):
-    """The 64-column band kernel (TSB_DCT_BAND=64, two CTAs per SM; the
-    default is 128-column bands) against the oracle."""
-    monkeypatch.setenv("TSB_DCT_BAND", "64")
+def test_full_band_variant_matches_oracle(shape, monkeypatch):
+    """The 128-column band kernel (TSB_DCT_BAND=128, one CTA per SM; the
+    default is 64-column bands, two CTAs per SM) against the oracle."""
+    monkeypatch.setenv("TSB_DCT_BAND", "128")
     x = _noisy(shape, 5)
     y = _gpu(x, threshold=0.15, mode="soft")
     ref = pipelines_ref.dct_denoise(x, 0.15, "soft")
