@@ -5,8 +5,9 @@
 // windowed synthesis overlap-adds to the identity), coring in the transform
 // domain (hard or soft threshold; DC kept), clamp-to-edge outside the image.
 //
-// One persistent CTA per SM; work unit = a 128x128 input band at image
-// offset (Y-8, X-8) producing the 112x112 output block (Y.., X..).  The 15
+// Persistent CTAs (two per SM with the default 64-column bands, one with
+// 128-column bands); work unit = a 128 x BW input band at image offset
+// (Y-8, X-8) producing the 112 x (BW-16) output block (Y.., X..).  The 15
 // tile rows of the band (tile row t starts at band row 8t) split into two
 // groups g (t = 8g .. 8g+7) that run the chain one after the other; column
 // phases q are tiles at band columns 16j+8q.  Per group, with
