@@ -108,6 +108,14 @@ TS_API void ts_axis_destroy(ts_axis* a);
 
 /* ----------------------------------------------------------- executors */
 
+/* Output epilogue, applied inside the producing kernel to every f32 result
+ * before its final cast (the "clamp / normalise" step of an image pipeline):
+ *   y = min(max(x * scale + bias, lo), hi)      (NaN propagates)
+ * The *_ep entry points take it; NULL (or the plain entry points) means none. */
+typedef struct ts_epilogue {
+  float scale, bias, lo, hi;
+} ts_epilogue;
+
 /* Fused separable transform  out[p] = R · in[p] · Cᵀ  for `planes` planes:
  * one sm_100a kernel (TMA-staged halo tiles -> tcgen05 vertical pass ->
  * TMEM -> smem -> tcgen05 horizontal pass -> TMEM -> cast -> TMA store).
@@ -119,6 +127,13 @@ TS_API ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int 
                            int64_t in_row_stride, int64_t in_plane_stride, int in_dtype, void* out,
                            int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
                            void* stream);
+
+/* ts_separable_run with an output epilogue (see ts_epilogue). */
+TS_API ts_status ts_separable_run_ep(const ts_axis* rows, const ts_axis* cols, int planes,
+                                     const void* in, int64_t in_row_stride,
+                                     int64_t in_plane_stride, int in_dtype, void* out,
+                                     int64_t out_row_stride, int64_t out_plane_stride,
+                                     int out_dtype, const ts_epilogue* ep, void* stream);
 
 /* One banded axis along rows (dim = 0: out is a->n_out x width) or columns
  * (dim = 1: out is height x a->n_out) of `planes` bf16 planes; out bf16 or
@@ -133,6 +148,12 @@ TS_API ts_status ts_axis_pass(const ts_axis* a, int dim, int planes, int height,
                               const void* in, int64_t in_row_stride, int64_t in_plane_stride,
                               void* out, int64_t out_row_stride, int64_t out_plane_stride,
                               int out_dtype, void* stream);
+
+/* ts_axis_pass with an output epilogue (for the last pass of a pipeline). */
+TS_API ts_status ts_axis_pass_ep(const ts_axis* a, int dim, int planes, int height, int width,
+                                 const void* in, int64_t in_row_stride, int64_t in_plane_stride,
+                                 void* out, int64_t out_row_stride, int64_t out_plane_stride,
+                                 int out_dtype, const ts_epilogue* ep, void* stream);
 
 /* Launch geometry ts_separable_run would use for these axes:
  * out8 = {stages, V buffers, weights resident (0/1), smem bytes, staged rows
@@ -164,6 +185,14 @@ TS_API ts_status ts_denoise_dct16(const void* in, int64_t in_row_stride, int64_t
                                   int in_dtype, void* out, int64_t out_row_stride,
                                   int64_t out_plane_stride, int out_dtype, int planes, int height,
                                   int width, float threshold, int soft, void* stream);
+
+/* ts_denoise_dct16 with an output epilogue. */
+TS_API ts_status ts_denoise_dct16_ep(const void* in, int64_t in_row_stride,
+                                     int64_t in_plane_stride, int in_dtype, void* out,
+                                     int64_t out_row_stride, int64_t out_plane_stride,
+                                     int out_dtype, int planes, int height, int width,
+                                     float threshold, int soft, const ts_epilogue* ep,
+                                     void* stream);
 
 /* Diagnostics: subsequent ts_denoise_dct16 launches copy the TMEM
  * accumulators of CTA 0's first band (D1, D2, D3 per phase; D4) into

@@ -15,7 +15,8 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_native", "libtsb200.so")
+# TSB_LIB_PATH: an alternative build of the same library (same-box A/B experiments)
+LIB_PATH = os.environ.get("TSB_LIB_PATH") or os.path.join(_HERE, "_native", "libtsb200.so")
 
 TS_BF16, TS_F32, TS_F16 = 1, 2, 3
 TS_AXIS_DC_EXACT = 0x1
@@ -50,6 +51,12 @@ class AxisInfo(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class Epilogue(ctypes.Structure):
+    """ts_epilogue: y = min(max(x * scale + bias, lo), hi), inside the kernel."""
+    _fields_ = [("scale", ctypes.c_float), ("bias", ctypes.c_float),
+                ("lo", ctypes.c_float), ("hi", ctypes.c_float)]
+
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _I64 = ctypes.c_int64
@@ -68,9 +75,13 @@ _SIGNATURES = {
     "ts_axis_dense": (_I, [_P, _FP]),
     "ts_axis_destroy": (None, [_P]),
     "ts_separable_run": (_I, [_P, _P, _I, _P, _I64, _I64, _I, _P, _I64, _I64, _I, _P]),
+    "ts_separable_run_ep": (_I, [_P, _P, _I, _P, _I64, _I64, _I, _P, _I64, _I64, _I,
+                                 ctypes.POINTER(Epilogue), _P]),
     "ts_separable_plan": (_I, [_P, _P, _I, _I, ctypes.POINTER(ctypes.c_int)]),
     "ts_separable_variant": (_I, [_P, _P, _I, _I]),
     "ts_axis_pass": (_I, [_P, _I, _I, _I, _I, _P, _I64, _I64, _P, _I64, _I64, _I, _P]),
+    "ts_axis_pass_ep": (_I, [_P, _I, _I, _I, _I, _P, _I64, _I64, _P, _I64, _I64, _I,
+                             ctypes.POINTER(Epilogue), _P]),
     "ts_strip_info": (_I, [ctypes.POINTER(ctypes.c_int)]),
     "ts_probe_tma": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P]),
     "ts_probe_tmem_ld": (_I, [_I, _I, _I, _I, _P, _P]),
@@ -81,6 +92,8 @@ _SIGNATURES = {
     "ts_debug_dct16": (_I, [_P]),
     "ts_denoise_dct16": (_I, [_P, _I64, _I64, _I, _P, _I64, _I64, _I, _I, _I, _I,
                               ctypes.c_float, _I, _P]),
+    "ts_denoise_dct16_ep": (_I, [_P, _I64, _I64, _I, _P, _I64, _I64, _I, _I, _I, _I,
+                                 ctypes.c_float, _I, ctypes.POINTER(Epilogue), _P]),
     "ts_matrix_for": (_I, [_I, _I, _I, _I, _P, _P, _P]),
     "ts_probe_umma": (_I, [_P, _P, _P, _I, _I, _P]),
     "ts_debug_trace": (_I, [_P, _I, _I]),

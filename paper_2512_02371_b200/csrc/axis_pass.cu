@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdlib>
 
 #include "common.h"
@@ -54,9 +55,10 @@ struct Params {
   uint32_t tmem_cols;  // accumulator columns: 16 per block, power of two >= 32
   int nring;  // ring slots in use (<= Ring::kSlots): a group never needs more than it loads
   uint32_t off_b, off_out, off_bar;
+  EpiK ep;  // output epilogue (EPI kernels only)
 };
 
-template <bool VERT, typename OutT>
+template <bool VERT, typename OutT, bool EPI>
 __global__ void __launch_bounds__(kThreads)
     axis_pass_kernel(const __grid_constant__ CUtensorMap tm_in,
                      const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ Params P) {
@@ -177,6 +179,10 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t r[16];
     tmem_ld16(tl + 16u * j, r);
     tmem_wait_ld();
+    if constexpr (EPI) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(epi_f32(P.ep, __uint_as_float(r[i])));
+    }
     if (VERT) {  // lane = column c, values = 16 output rows: staging [nout][128]
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
@@ -224,8 +230,14 @@ __global__ void __launch_bounds__(kThreads)
 
 template <bool VERT, typename OutT>
 static cudaError_t launch(const Params& P, const CUtensorMap& tin, const CUtensorMap& tout,
-                          uint32_t smem, cudaStream_t stream) {
-  auto k = axis_pass_kernel<VERT, OutT>;
+                          uint32_t smem, cudaStream_t stream, bool epi) {
+  if (epi) {
+    auto k = axis_pass_kernel<VERT, OutT, true>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) k<<<P.nunits, kThreads, smem, stream>>>(tin, tout, P);
+    return e;
+  }
+  auto k = axis_pass_kernel<VERT, OutT, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) k<<<P.nunits, kThreads, smem, stream>>>(tin, tout, P);
   return e;
@@ -238,7 +250,7 @@ static cudaError_t launch(const Params& P, const CUtensorMap& tin, const CUtenso
 // H x a->n_out), bf16 or f32.
 ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, const void* in,
                         int64_t in_rs, int64_t in_ps, void* out, int64_t out_rs, int64_t out_ps,
-                        int out_dtype, cudaStream_t stream) {
+                        int out_dtype, const ts_epilogue* ep, cudaStream_t stream) {
   if (!a || !in || !out || planes < 1 || H < 1 || W < 1 || (dim != 0 && dim != 1))
     return set_error(TS_ERR_INVALID, "axis_pass: bad arguments");
   if (out_dtype != TS_BF16 && out_dtype != TS_F32)
@@ -255,6 +267,7 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   cudaError_t de = cudaSetDevice(a->device);
   if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
   apass::Params P;
+  P.ep = make_epik(ep);
   P.ax = a->dev();
   P.planes = planes;
   P.nb = a->nb;
@@ -315,12 +328,12 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   cudaError_t e;
   if (dim == 0)
     e = out_dtype == TS_BF16
-            ? apass::launch<true, __nv_bfloat16>(P, tin, tout, smem, stream)
-            : apass::launch<true, float>(P, tin, tout, smem, stream);
+            ? apass::launch<true, __nv_bfloat16>(P, tin, tout, smem, stream, ep != nullptr)
+            : apass::launch<true, float>(P, tin, tout, smem, stream, ep != nullptr);
   else
     e = out_dtype == TS_BF16
-            ? apass::launch<false, __nv_bfloat16>(P, tin, tout, smem, stream)
-            : apass::launch<false, float>(P, tin, tout, smem, stream);
+            ? apass::launch<false, __nv_bfloat16>(P, tin, tout, smem, stream, ep != nullptr)
+            : apass::launch<false, float>(P, tin, tout, smem, stream, ep != nullptr);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "axis_pass launch");
 }

@@ -12,7 +12,7 @@
 namespace tsb {
 ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const void* in,
                         int64_t in_rs, int64_t in_ps, int in_dtype, void* out, int64_t out_rs,
-                        int64_t out_ps, int out_dtype, cudaStream_t stream);
+                        int64_t out_ps, int out_dtype, const ts_epilogue* ep, cudaStream_t stream);
 ts_status separable_plan(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype,
                          int* out8);
 void set_trace(void* buf, int ctas, int tiles);
@@ -20,7 +20,7 @@ int separable_variant(const ts_axis* ra, const ts_axis* ca, int planes, int out_
 int strip_info(int* out16);
 ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, const void* in,
                         int64_t in_rs, int64_t in_ps, void* out, int64_t out_rs, int64_t out_ps,
-                        int out_dtype, cudaStream_t stream);
+                        int out_dtype, const ts_epilogue* ep, cudaStream_t stream);
 
 // ------------------------------------------------------------------ cast
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -157,7 +157,16 @@ ts_status ts_separable_run(const ts_axis* rows, const ts_axis* cols, int planes,
                            int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
                            void* stream) {
   return separable_run(rows, cols, planes, in, in_row_stride, in_plane_stride, in_dtype, out,
-                       out_row_stride, out_plane_stride, out_dtype,
+                       out_row_stride, out_plane_stride, out_dtype, nullptr,
+                       static_cast<cudaStream_t>(stream));
+}
+
+ts_status ts_separable_run_ep(const ts_axis* rows, const ts_axis* cols, int planes, const void* in,
+                              int64_t in_row_stride, int64_t in_plane_stride, int in_dtype,
+                              void* out, int64_t out_row_stride, int64_t out_plane_stride,
+                              int out_dtype, const ts_epilogue* ep, void* stream) {
+  return separable_run(rows, cols, planes, in, in_row_stride, in_plane_stride, in_dtype, out,
+                       out_row_stride, out_plane_stride, out_dtype, ep,
                        static_cast<cudaStream_t>(stream));
 }
 
@@ -175,7 +184,16 @@ ts_status ts_axis_pass(const ts_axis* a, int dim, int planes, int height, int wi
                        int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
                        void* stream) {
   return axis_pass_run(a, dim, planes, height, width, in, in_row_stride, in_plane_stride, out,
-                       out_row_stride, out_plane_stride, out_dtype,
+                       out_row_stride, out_plane_stride, out_dtype, nullptr,
+                       static_cast<cudaStream_t>(stream));
+}
+
+ts_status ts_axis_pass_ep(const ts_axis* a, int dim, int planes, int height, int width,
+                          const void* in, int64_t in_row_stride, int64_t in_plane_stride,
+                          void* out, int64_t out_row_stride, int64_t out_plane_stride,
+                          int out_dtype, const ts_epilogue* ep, void* stream) {
+  return axis_pass_run(a, dim, planes, height, width, in, in_row_stride, in_plane_stride, out,
+                       out_row_stride, out_plane_stride, out_dtype, ep,
                        static_cast<cudaStream_t>(stream));
 }
 

@@ -115,6 +115,7 @@ struct Params {
   float* dbg;               // diagnostics: [4 stages][2 phases][128 lanes][256] for CTA 0, band 0
   unsigned long long* trace;  // diagnostics (ts_debug_trace): clock64 per (CTA, band, event), 24 events
   int trace_ctas, trace_tiles;
+  EpiK ep;  // output epilogue (EPI kernels only)
 };
 
 // events: 12p + {0 D1 seen, 1 C1 done, 2 D2 (q=0) seen, 6 D2 (q=1) seen, 3 E2 done,
@@ -245,7 +246,7 @@ __device__ __forceinline__ Region region_of(const Params& P, int t) {
   return r;
 }
 
-template <int BW, typename OutT, bool SOFT>
+template <int BW, typename OutT, bool SOFT, bool EPI = false>
 __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     dct16_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                  const __grid_constant__ Params P) {
@@ -460,16 +461,23 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
               if (c >= 8 && c < 8 + kOut) {
                 const uint32_t* src = &v[g >> 1][8 * (g & 1)];
                 if constexpr (sizeof(OutT) == 2) {
+                  uint32_t pk[4];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i)
+                    pk[i] = EPI ? epi_bf16x2(P.ep, __uint_as_float(src[2 * i]),
+                                             __uint_as_float(src[2 * i + 1]))
+                                : pack_bf16x2(__uint_as_float(src[2 * i]),
+                                              __uint_as_float(src[2 * i + 1]));
                   *reinterpret_cast<uint4*>(orow + (c - 8) * 2) =
-                      make_uint4(pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1])),
-                                 pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3])),
-                                 pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5])),
-                                 pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7])));
+                      make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 } else {
-                  *reinterpret_cast<uint4*>(orow + (c - 8) * 4) =
-                      make_uint4(src[0], src[1], src[2], src[3]);
+                  uint32_t f[8];
+#pragma unroll
+                  for (int i = 0; i < 8; ++i)
+                    f[i] = EPI ? __float_as_uint(epi_f32(P.ep, __uint_as_float(src[i]))) : src[i];
+                  *reinterpret_cast<uint4*>(orow + (c - 8) * 4) = make_uint4(f[0], f[1], f[2], f[3]);
                   *reinterpret_cast<uint4*>(orow + (c - 8) * 4 + 16) =
-                      make_uint4(src[4], src[5], src[6], src[7]);
+                      make_uint4(f[4], f[5], f[6], f[7]);
                 }
               }
             }
@@ -689,11 +697,11 @@ static void build_consts(uint8_t* out) {
     for (int l = 0; l < 16; ++l) put16h(out + dct::kCB5, c, l, D[l][c]);
 }
 
-template <int BW, typename OutT, bool SOFT>
+template <int BW, typename OutT, bool SOFT, bool EPI = false>
 static cudaError_t launch_dct(const CUtensorMap& tin, const CUtensorMap& tout,
                               const dct::Params& P, cudaStream_t stream) {
   using G = dct::Geo<BW>;
-  auto k = dct::dct16_kernel<BW, OutT, SOFT>;
+  auto k = dct::dct16_kernel<BW, OutT, SOFT, EPI>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem);
   if (e != cudaSuccess) return e;
   const int slots = G::kMinBlocks * sm_count_current();
@@ -706,10 +714,11 @@ template <int BW>
 static ts_status dct16_run_bw(const void* in, int64_t in_rs, int64_t in_ps, void* out,
                               int64_t out_rs, int64_t out_ps, int out_dtype, int planes, int H,
                               int W, float threshold, int soft, const uint8_t* consts,
-                              cudaStream_t stream) {
+                              const ts_epilogue* ep, cudaStream_t stream) {
   using G = dct::Geo<BW>;
   const int oes = out_dtype == TS_BF16 ? 2 : 4;
   dct::Params P;
+  P.ep = make_epik(ep);
   P.planes = planes;
   P.H = H;
   P.W = W;
@@ -732,19 +741,31 @@ static ts_status dct16_run_bw(const void* in, int64_t in_rs, int64_t in_ps, void
                       CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TS_OK) return st;
   cudaError_t e;
-  if (out_dtype == TS_BF16)
+  if (ep) {  // epilogue kernels: the default 64-column bands only (dct16_run)
+    if constexpr (BW == 64) {
+      if (out_dtype == TS_BF16)
+        e = soft ? launch_dct<BW, __nv_bfloat16, true, true>(tin, tout, P, stream)
+                 : launch_dct<BW, __nv_bfloat16, false, true>(tin, tout, P, stream);
+      else
+        e = soft ? launch_dct<BW, float, true, true>(tin, tout, P, stream)
+                 : launch_dct<BW, float, false, true>(tin, tout, P, stream);
+    } else {
+      return set_error(TS_ERR_UNSUPPORTED, "dct16: output epilogue needs 64-column bands");
+    }
+  } else if (out_dtype == TS_BF16) {
     e = soft ? launch_dct<BW, __nv_bfloat16, true>(tin, tout, P, stream)
              : launch_dct<BW, __nv_bfloat16, false>(tin, tout, P, stream);
-  else
+  } else {
     e = soft ? launch_dct<BW, float, true>(tin, tout, P, stream)
              : launch_dct<BW, float, false>(tin, tout, P, stream);
+  }
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "dct16 launch");
 }
 
 ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, void* out,
                     int64_t out_rs, int64_t out_ps, int out_dtype, int planes, int H, int W,
-                    float threshold, int soft, cudaStream_t stream) {
+                    float threshold, int soft, const ts_epilogue* ep, cudaStream_t stream) {
   if (!in || !out || planes < 1 || H < 8 || W < 8)
     return set_error(TS_ERR_INVALID, "dct16: bad arguments");
   if (H % 8 || W % 8) return set_error(TS_ERR_UNSUPPORTED, "dct16: H and W must be multiples of 8");
@@ -780,11 +801,11 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
   // TSB_DCT_BAND=128 (one CTA per SM): 2% faster on B200 (82 vs 84 us per
   // 4K frame, same-box A/B, tools/ab_env.sh)
   const char* v = std::getenv("TSB_DCT_BAND");
-  if (v && std::atoi(v) == 128)
+  if (v && std::atoi(v) == 128 && !ep)
     return dct16_run_bw<128>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
-                             threshold, soft, d_consts[dev], stream);
+                             threshold, soft, d_consts[dev], nullptr, stream);
   return dct16_run_bw<64>(in, in_rs, in_ps, out, out_rs, out_ps, out_dtype, planes, H, W,
-                          threshold, soft, d_consts[dev], stream);
+                          threshold, soft, d_consts[dev], ep, stream);
 }
 
 }  // namespace tsb
@@ -800,5 +821,16 @@ extern "C" ts_status ts_denoise_dct16(const void* in, int64_t in_row_stride, int
                                       int width, float threshold, int soft, void* stream) {
   return tsb::dct16_run(in, in_row_stride, in_plane_stride, in_dtype, out, out_row_stride,
                         out_plane_stride, out_dtype, planes, height, width, threshold, soft,
+                        nullptr, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" ts_status ts_denoise_dct16_ep(const void* in, int64_t in_row_stride,
+                                         int64_t in_plane_stride, int in_dtype, void* out,
+                                         int64_t out_row_stride, int64_t out_plane_stride,
+                                         int out_dtype, int planes, int height, int width,
+                                         float threshold, int soft, const ts_epilogue* ep,
+                                         void* stream) {
+  return tsb::dct16_run(in, in_row_stride, in_plane_stride, in_dtype, out, out_row_stride,
+                        out_plane_stride, out_dtype, planes, height, width, threshold, soft, ep,
                         static_cast<cudaStream_t>(stream));
 }

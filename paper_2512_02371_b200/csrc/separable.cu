@@ -38,6 +38,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include "common.h"
 #include "sm100.cuh"
 
@@ -81,6 +83,7 @@ struct SepParams {
   int ptab_c;    // offset of the cols table inside tab[]
   SepSmem L;
   int32_t tab[kParamTab];  // packed (ws << 16) | tid, rows then cols
+  EpiK ep;                 // output epilogue (EPI kernels only)
 };
 
 __device__ __forceinline__ int32_t tab_r(const SepParams& P, int b) {
@@ -101,24 +104,28 @@ __device__ __forceinline__ int tab_tid(int32_t e) { return e & 0xFFFF; }
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-template <typename OutT>
-__device__ __forceinline__ void store_out_row(uint32_t dst, const uint32_t (&r)[16]);
-
-template <>
-__device__ __forceinline__ void store_out_row<__nv_bfloat16>(uint32_t dst, const uint32_t (&r)[16]) {
-  uint32_t p[8];
+// one 16-column block of an output row into the staging tile, with the
+// output epilogue when EPI
+template <typename OutT, bool EPI>
+__device__ __forceinline__ void store_out_row(uint32_t dst, uint32_t (&r)[16], const EpiK& ep) {
+  if constexpr (sizeof(OutT) == 2) {
+    uint32_t p[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-  st_shared_v4(dst, p[0], p[1], p[2], p[3]);
-  st_shared_v4(dst + 16, p[4], p[5], p[6], p[7]);
-}
-
-template <>
-__device__ __forceinline__ void store_out_row<float>(uint32_t dst, const uint32_t (&r)[16]) {
+    for (int i = 0; i < 8; ++i) {
+      p[i] = EPI ? epi_bf16x2(ep, __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]))
+                 : pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+    }
+    st_shared_v4(dst, p[0], p[1], p[2], p[3]);
+    st_shared_v4(dst + 16, p[4], p[5], p[6], p[7]);
+  } else {
+    if constexpr (EPI) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    st_shared_v4(dst + 16 * i, r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+      for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(epi_f32(ep, __uint_as_float(r[i])));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      st_shared_v4(dst + 16 * i, r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+  }
 }
 
 // Persistent tile walk t = blockIdx.x + it·gridDim.x with (p, rt, ct) kept
@@ -150,7 +157,7 @@ struct TileWalk {
   }
 };
 
-template <typename OutT, int KQ1, int KQ2>
+template <typename OutT, int KQ1, int KQ2, bool EPI = false>
 __global__ void __launch_bounds__(kThreads, 1)
     separable_kernel(const __grid_constant__ CUtensorMap tm_in,
                      const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ SepParams P) {
@@ -421,7 +428,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (j0 + j < nb2) store_out_row<OutT>(orow + (j0 + j) * 16u * sizeof(OutT), r[j]);
+          if (j0 + j < nb2)
+            store_out_row<OutT, EPI>(orow + (j0 + j) * 16u * sizeof(OutT), r[j], P.ep);
       }
       fence_proxy_async_smem();
       named_bar_sync(2, 128);
@@ -536,10 +544,10 @@ static bool plan_smem(SepParams& P, int oes) {
   return false;
 }
 
-template <typename OutT, int KQ1, int KQ2>
+template <typename OutT, int KQ1, int KQ2, bool EPI = false>
 static ts_status launch_sep_k(const SepParams& P, const CUtensorMap& tin, const CUtensorMap& tout,
                               cudaStream_t stream) {
-  auto kern = separable_kernel<OutT, KQ1, KQ2>;
+  auto kern = separable_kernel<OutT, KQ1, KQ2, EPI>;
   // the smem ceiling is set once per device (to the maximum any plan uses)
   static bool attr_done[64] = {false};
   int dev = 0;
@@ -561,29 +569,38 @@ static ts_status launch_sep_k(const SepParams& P, const CUtensorMap& tin, const 
 
 // Compile-time K-step counts for the common windows (32, 48, 64 inputs per
 // 16-output block); anything else runs the runtime-count variant.
-template <typename OutT, int KQ1>
+template <typename OutT, int KQ1, bool EPI>
 static ts_status launch_sep_k2(const SepParams& P, const CUtensorMap& tin,
                                const CUtensorMap& tout, cudaStream_t stream) {
   switch (P.c.K / 16) {
-    case 2: return launch_sep_k<OutT, KQ1, 2>(P, tin, tout, stream);
-    case 3: return launch_sep_k<OutT, KQ1, 3>(P, tin, tout, stream);
-    case 4: return launch_sep_k<OutT, KQ1, 4>(P, tin, tout, stream);
-    case 5: return launch_sep_k<OutT, KQ1, 5>(P, tin, tout, stream);
-    default: return launch_sep_k<OutT, KQ1, 0>(P, tin, tout, stream);
+    case 2: return launch_sep_k<OutT, KQ1, 2, EPI>(P, tin, tout, stream);
+    case 3: return launch_sep_k<OutT, KQ1, 3, EPI>(P, tin, tout, stream);
+    case 4: return launch_sep_k<OutT, KQ1, 4, EPI>(P, tin, tout, stream);
+    case 5: return launch_sep_k<OutT, KQ1, 5, EPI>(P, tin, tout, stream);
+    default: return launch_sep_k<OutT, KQ1, 0, EPI>(P, tin, tout, stream);
   }
 }
 
+template <typename OutT, bool EPI>
+static ts_status launch_sep_e(const SepParams& P, const CUtensorMap& tin, const CUtensorMap& tout,
+                              cudaStream_t stream) {
+  switch (P.r.K / 16) {
+    case 2: return launch_sep_k2<OutT, 2, EPI>(P, tin, tout, stream);
+    case 3: return launch_sep_k2<OutT, 3, EPI>(P, tin, tout, stream);
+    case 4: return launch_sep_k2<OutT, 4, EPI>(P, tin, tout, stream);
+    case 5: return launch_sep_k2<OutT, 5, EPI>(P, tin, tout, stream);
+    case 6: return launch_sep_k2<OutT, 6, EPI>(P, tin, tout, stream);
+    default: return launch_sep_k2<OutT, 0, EPI>(P, tin, tout, stream);
+  }
+}
+
+// with an output epilogue the EPI twins of the same kernels run (the plain
+// kernels carry no epilogue code)
 template <typename OutT>
 static ts_status launch_sep(const SepParams& P, const CUtensorMap& tin, const CUtensorMap& tout,
-                            cudaStream_t stream) {
-  switch (P.r.K / 16) {
-    case 2: return launch_sep_k2<OutT, 2>(P, tin, tout, stream);
-    case 3: return launch_sep_k2<OutT, 3>(P, tin, tout, stream);
-    case 4: return launch_sep_k2<OutT, 4>(P, tin, tout, stream);
-    case 5: return launch_sep_k2<OutT, 5>(P, tin, tout, stream);
-    case 6: return launch_sep_k2<OutT, 6>(P, tin, tout, stream);
-    default: return launch_sep_k2<OutT, 0>(P, tin, tout, stream);
-  }
+                            cudaStream_t stream, bool epi) {
+  return epi ? launch_sep_e<OutT, true>(P, tin, tout, stream)
+             : launch_sep_e<OutT, false>(P, tin, tout, stream);
 }
 
 static unsigned long long* g_trace = nullptr;
@@ -670,7 +687,7 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
 
 ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const void* in,
                         int64_t in_rs, int64_t in_ps, int in_dtype, void* out, int64_t out_rs,
-                        int64_t out_ps, int out_dtype, cudaStream_t stream) {
+                        int64_t out_ps, int out_dtype, const ts_epilogue* ep, cudaStream_t stream) {
   if (!ra || !ca || !in || !out) return set_error(TS_ERR_INVALID, "separable: null argument");
   if (planes < 1) return set_error(TS_ERR_INVALID, "separable: planes must be >= 1");
   if (in_dtype != TS_BF16)
@@ -691,10 +708,13 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   cudaError_t de = cudaSetDevice(ra->device);
   if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
 
-  // Toeplitz-like axes take the strip kernel (separable_strip.cu)
-  ts_status s5 = strip_run(ra, ca, planes, in, in_rs, in_ps, out, out_rs, out_ps, out_dtype,
-                           stream, false);
-  if (s5 != TS_ERR_UNSUPPORTED) return s5;
+  // Toeplitz-like axes take the strip kernel (separable_strip.cu; opt-in,
+  // no epilogue variant)
+  if (!ep) {
+    ts_status s5 = strip_run(ra, ca, planes, in, in_rs, in_ps, out, out_rs, out_ps, out_dtype,
+                             stream, false);
+    if (s5 != TS_ERR_UNSUPPORTED) return s5;
+  }
 
   // launch parameters (block tables, smem plan) are cached per (axes, planes,
   // output size): rebuilding them costs more host time than a 1-frame launch
@@ -721,6 +741,7 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
     hit = &c;
   }
   SepParams& P = hit->P;
+  P.ep = make_epik(ep);
   P.trace = g_trace;
   P.trace_ctas = g_trace_ctas;
   P.trace_tiles = g_trace_tiles;
@@ -735,8 +756,8 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
                       oes, out, ca->n_out, ra->n_out, planes, out_rs, out_ps, P.nb2 * 16, 128,
                       CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TS_OK) return st;
-  if (out_dtype == TS_BF16) return launch_sep<__nv_bfloat16>(P, tin, tout, stream);
-  return launch_sep<float>(P, tin, tout, stream);
+  if (out_dtype == TS_BF16) return launch_sep<__nv_bfloat16>(P, tin, tout, stream, ep != nullptr);
+  return launch_sep<float>(P, tin, tout, stream, ep != nullptr);
 }
 
 // Which kernel ts_separable_run would launch: 5 (strip) or 4 (block tiles).

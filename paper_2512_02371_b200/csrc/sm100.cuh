@@ -7,9 +7,12 @@
 // fields CuTe's UMMA::SmemDescriptor / UMMA::InstrDescriptor spell out).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+
+#include "../../include/tensorsel_b200.h"
 
 namespace tsb {
 
@@ -304,9 +307,47 @@ enum : uint32_t { kFmtF16 = 0, kFmtBF16 = 1, kFmtTF32 = 2 };
 // ---------------------------------------------------------------------------
 // small conversions
 
+// Output epilogue (ts_epilogue): y = min(max(x * scale + bias, lo), hi),
+// NaN-propagating min / max.  The kernels carry the user's ts_epilogue plus
+// the bounds pre-rounded to a bf16 pair: for bf16 outputs the clamp runs on
+// the packed pair (one max + one min per two values) — RNE rounding is
+// monotone, so rounding then clamping to the rounded bounds equals rounding
+// the clamped f32 value, bit for bit.  The multiply-add always runs: a
+// data-independent branch around it cost c2 a quarter of its time on B200
+// (24% vs 2.4% epilogue overhead, same-box A/B, tools/time_epilogue.py).
+struct EpiK {
+  ts_epilogue e;
+  uint32_t lo2, hi2;  // bf16x2 (RNE) of e.lo / e.hi
+};
+
+inline EpiK make_epik(const ts_epilogue* ep) {
+  EpiK k;
+  k.e = ep ? *ep : ts_epilogue{1.0f, 0.0f, -INFINITY, INFINITY};
+  const uint16_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(k.e.lo));
+  const uint16_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(k.e.hi));
+  k.lo2 = lo | (static_cast<uint32_t>(lo) << 16);
+  k.hi2 = hi | (static_cast<uint32_t>(hi) << 16);
+  return k;
+}
+
+__device__ __forceinline__ float epi_f32(const EpiK& k, float x) {
+  x = fmaf(x, k.e.scale, k.e.bias);
+  asm("max.NaN.f32 %0, %0, %1;" : "+f"(x) : "f"(k.e.lo));
+  asm("min.NaN.f32 %0, %0, %1;" : "+f"(x) : "f"(k.e.hi));
+  return x;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// pack_bf16x2 with the epilogue (see EpiK)
+__device__ __forceinline__ uint32_t epi_bf16x2(const EpiK& k, float lo, float hi) {
+  uint32_t p = pack_bf16x2(fmaf(lo, k.e.scale, k.e.bias), fmaf(hi, k.e.scale, k.e.bias));
+  asm("max.NaN.bf16x2 %0, %0, %1;" : "+r"(p) : "r"(k.lo2));
+  asm("min.NaN.bf16x2 %0, %0, %1;" : "+r"(p) : "r"(k.hi2));
+  return p;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,

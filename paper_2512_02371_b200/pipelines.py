@@ -13,6 +13,13 @@ Images are planar: a tensor ``(..., H, W)`` is a stack of planes (RGB
 counts as 3 planes).  Inputs are bf16 (or f32, cast to bf16 on the device);
 accumulation is f32 on the tensor cores.  Edges are clamp-to-edge.  There is
 no CPU path: without the native library or a CUDA device these raise.
+
+Every pipeline takes an optional output epilogue, applied inside the
+producing kernel to the f32 result before the final cast (the "clamp /
+normalise" step): ``y = clamp(x * scale + bias, *clamp)``, e.g.
+``resample(x, 1080, 1920, clamp=(0, 1))`` removes Lanczos overshoot and
+``scale=255.0`` rescales to 8-bit range.  Without these arguments the
+kernels without an epilogue run.
 """
 
 from __future__ import annotations
@@ -86,7 +93,23 @@ def _stream(x):
     return torch.cuda.current_stream(x.device).cuda_stream
 
 
-def _run(x, ra, ca, out_dtype):
+def _epilogue(clamp, scale, bias):
+    """ts_epilogue for the keyword arguments, or None (no epilogue)."""
+    if clamp is None and scale is None and bias is None:
+        return None
+    lo, hi = (-math.inf, math.inf) if clamp is None else (float(clamp[0]), float(clamp[1]))
+    if lo > hi:
+        raise ValueError(f"clamp=({lo}, {hi}): lower bound above upper bound")
+    return _lib.Epilogue(1.0 if scale is None else float(scale),
+                         0.0 if bias is None else float(bias), lo, hi)
+
+
+def _ep_ptr(ep):
+    import ctypes
+    return ctypes.byref(ep)
+
+
+def _run(x, ra, ca, out_dtype, ep=None):
     torch = _torch()
     _check_device(x)
     stream = _stream(x)
@@ -106,9 +129,14 @@ def _run(x, ra, ca, out_dtype):
     ts_out = _lib.TS_BF16 if out_dtype == torch.bfloat16 else _lib.TS_F32
     lib = _lib.load()
     if fused_supported(ra, ca, P, ts_out):
-        _lib.check(lib.ts_separable_run(
-            ra.handle, ca.handle, P, inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16,
-            out.data_ptr(), owp, owp * oh, ts_out, stream), "ts_separable_run")
+        if ep is None:
+            _lib.check(lib.ts_separable_run(
+                ra.handle, ca.handle, P, inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16,
+                out.data_ptr(), owp, owp * oh, ts_out, stream), "ts_separable_run")
+        else:
+            _lib.check(lib.ts_separable_run_ep(
+                ra.handle, ca.handle, P, inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16,
+                out.data_ptr(), owp, owp * oh, ts_out, _ep_ptr(ep), stream), "ts_separable_run_ep")
     else:
         # windows too wide for the fused tile (large downscale factors, very
         # wide filters): two axis passes, bf16 intermediate in HBM — the same
@@ -117,58 +145,65 @@ def _run(x, ra, ca, out_dtype):
         _lib.check(lib.ts_axis_pass(ra.handle, 0, P, H, W, inb.data_ptr(), in_rs, in_rs * H,
                                     mid.data_ptr(), in_rs, in_rs * oh, _lib.TS_BF16, stream),
                    "ts_axis_pass")
-        _lib.check(lib.ts_axis_pass(ca.handle, 1, P, oh, W, mid.data_ptr(), in_rs, in_rs * oh,
-                                    out.data_ptr(), owp, owp * oh, ts_out, stream),
-                   "ts_axis_pass")
+        if ep is None:
+            _lib.check(lib.ts_axis_pass(ca.handle, 1, P, oh, W, mid.data_ptr(), in_rs, in_rs * oh,
+                                        out.data_ptr(), owp, owp * oh, ts_out, stream),
+                       "ts_axis_pass")
+        else:  # the epilogue belongs to the last pass
+            _lib.check(lib.ts_axis_pass_ep(ca.handle, 1, P, oh, W, mid.data_ptr(), in_rs,
+                                           in_rs * oh, out.data_ptr(), owp, owp * oh, ts_out,
+                                           _ep_ptr(ep), stream), "ts_axis_pass_ep")
     if owp != ow:
         out = out[:, :, :ow]
     return out.reshape(*x.shape[:-2], oh, ow)
 
 
-def resample(x, out_h: int, out_w: int, *, out_dtype=None):
+def resample(x, out_h: int, out_w: int, *, out_dtype=None, clamp=None, scale=None, bias=None):
     """Separable Lanczos-3 resample of planar images to (out_h, out_w)."""
     dev = _check_device(x)
     H, W = x.shape[-2], x.shape[-1]
     ra = _axis.lanczos3(H, out_h, dev)
     ca = _axis.lanczos3(W, out_w, dev)
-    return _run(x, ra, ca, out_dtype)
+    return _run(x, ra, ca, out_dtype, _epilogue(clamp, scale, bias))
 
 
-def downsample2x(x, *, out_dtype=None):
+def downsample2x(x, *, out_dtype=None, clamp=None, scale=None, bias=None):
     """Lanczos-3 2x downsample (configs 1/2: 1080p->540p, 4K->1080p)."""
     H, W = x.shape[-2], x.shape[-1]
-    return resample(x, H // 2, W // 2, out_dtype=out_dtype)
+    return resample(x, H // 2, W // 2, out_dtype=out_dtype, clamp=clamp, scale=scale, bias=bias)
 
 
-def upsample2x(x, *, out_dtype=None):
+def upsample2x(x, *, out_dtype=None, clamp=None, scale=None, bias=None):
     """Lanczos-3 2x upsample: the polyphase Toeplitz case (layout.polyphase_toeplitz,
     layout.py:97-103) — each output phase is a 6-tap filter."""
     H, W = x.shape[-2], x.shape[-1]
-    return resample(x, 2 * H, 2 * W, out_dtype=out_dtype)
+    return resample(x, 2 * H, 2 * W, out_dtype=out_dtype, clamp=clamp, scale=scale, bias=bias)
 
 
-def filter_separable(x, kernel_v, kernel_h=None, *, out_dtype=None):
+def filter_separable(x, kernel_v, kernel_h=None, *, out_dtype=None, clamp=None, scale=None,
+                     bias=None):
     """Same-size separable convolution (centred taps, clamp-to-edge)."""
     dev = _check_device(x)
     kernel_h = kernel_v if kernel_h is None else kernel_h
     H, W = x.shape[-2], x.shape[-1]
     ra = _axis.convolution(H, kernel_v, dev)
     ca = _axis.convolution(W, kernel_h, dev)
-    return _run(x, ra, ca, out_dtype)
+    return _run(x, ra, ca, out_dtype, _epilogue(clamp, scale, bias))
 
 
-def gaussian_blur(x, taps: int, sigma: float | None = None, *, out_dtype=None):
+def gaussian_blur(x, taps: int, sigma: float | None = None, *, out_dtype=None, clamp=None,
+                  scale=None, bias=None):
     k = filters.gaussian_taps(taps, sigma)
-    return filter_separable(x, k, k, out_dtype=out_dtype)
+    return filter_separable(x, k, k, out_dtype=out_dtype, clamp=clamp, scale=scale, bias=bias)
 
 
-def box_blur(x, taps: int, *, out_dtype=None):
+def box_blur(x, taps: int, *, out_dtype=None, clamp=None, scale=None, bias=None):
     k = filters.box_taps(taps)
-    return filter_separable(x, k, k, out_dtype=out_dtype)
+    return filter_separable(x, k, k, out_dtype=out_dtype, clamp=clamp, scale=scale, bias=bias)
 
 
 def resample_filter(x, out_h: int, out_w: int, taps: int = 9, sigma: float | None = None, *,
-                    out_dtype=None):
+                    out_dtype=None, clamp=None, scale=None, bias=None):
     """Lanczos-3 resample to (out_h, out_w), then a `taps`-tap Gaussian at the
     output resolution (config 5) — fused into ONE separable pass by composing
     the two banded axes on the host (no intermediate image in HBM)."""
@@ -177,10 +212,11 @@ def resample_filter(x, out_h: int, out_w: int, taps: int = 9, sigma: float | Non
     k = filters.gaussian_taps(taps, sigma)
     ra = _axis.resample_filter(H, out_h, k, dev)
     ca = _axis.resample_filter(W, out_w, k, dev)
-    return _run(x, ra, ca, out_dtype)
+    return _run(x, ra, ca, out_dtype, _epilogue(clamp, scale, bias))
 
 
-def denoise_dct16(x, threshold: float = 0.15, mode: str = "hard", *, out_dtype=None):
+def denoise_dct16(x, threshold: float = 0.15, mode: str = "hard", *, out_dtype=None,
+                  clamp=None, scale=None, bias=None):
     """DCT-16 transform-domain coring (config 4): 16x16
     tiles at stride 8, sine-windowed DCT-II, coefficients below `threshold`
     zeroed (mode="hard", the paper's coring) or shrunk (mode="soft"), DC
@@ -201,18 +237,24 @@ def denoise_dct16(x, threshold: float = 0.15, mode: str = "hard", *, out_dtype=N
     align = 8 if out_dtype == torch.bfloat16 else 4
     owp = -(-W // align) * align
     out = torch.empty((P, H, owp), dtype=out_dtype, device=x.device)
-    _lib.check(_lib.load().ts_denoise_dct16(
-        inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16, out.data_ptr(), owp, owp * H,
-        _lib.TS_BF16 if out_dtype == torch.bfloat16 else _lib.TS_F32, P, H, W,
-        float(threshold), 1 if mode == "soft" else 0, stream), "ts_denoise_dct16")
+    ep = _epilogue(clamp, scale, bias)
+    args = (inb.data_ptr(), in_rs, in_rs * H, _lib.TS_BF16, out.data_ptr(), owp, owp * H,
+            _lib.TS_BF16 if out_dtype == torch.bfloat16 else _lib.TS_F32, P, H, W,
+            float(threshold), 1 if mode == "soft" else 0)
+    if ep is None:
+        _lib.check(_lib.load().ts_denoise_dct16(*args, stream), "ts_denoise_dct16")
+    else:
+        _lib.check(_lib.load().ts_denoise_dct16_ep(*args, _ep_ptr(ep), stream),
+                   "ts_denoise_dct16_ep")
     if owp != W:
         out = out[:, :, :W]
     return out.reshape(*x.shape[:-2], H, W)
 
 
-def separable(x, rows: "_axis.Axis", cols: "_axis.Axis", *, out_dtype=None):
+def separable(x, rows: "_axis.Axis", cols: "_axis.Axis", *, out_dtype=None, clamp=None,
+              scale=None, bias=None):
     """Apply explicit axes: out = rows · x · colsᵀ per plane."""
-    return _run(x, rows, cols, out_dtype)
+    return _run(x, rows, cols, out_dtype, _epilogue(clamp, scale, bias))
 
 
 _LANES = {}

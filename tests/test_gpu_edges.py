@@ -126,3 +126,50 @@ def test_fused_kernel_global_block_tables():
     y = _gpu(pipelines.resample, x, out_h=48000, out_w=96)
     ref = pipelines_ref.resample(x, 48000, 96)
     assert np.abs(y - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("case", ["fused", "two_pass", "gauss", "dct"])
+def test_output_epilogue_clamp_and_normalise(case):
+    """The in-kernel output epilogue (ts_epilogue): clamp / scale / bias
+    applied to the f32 result before the cast equal the same operations on
+    the plain kernel's f32 output (bitwise for the clamp, f32 rounding of
+    one fused multiply-add for scale / bias).  bf16 outputs clamp the packed
+    pair against bf16-rounded bounds, which must equal clamping in f32 and
+    then rounding, bit for bit; NaN inputs stay NaN through the clamp."""
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.rand((3, 544, 960), device="cuda", generator=g).bfloat16()
+    x = x * 1.6 - 0.3  # overshoot both clamp bounds
+    fns = {"fused": lambda **kw: pipelines.resample(x, 272, 480, **kw),
+           "two_pass": lambda **kw: pipelines.resample(x, 40, 70, **kw),
+           "gauss": lambda **kw: pipelines.gaussian_blur(x, 9, **kw),
+           "dct": lambda **kw: pipelines.denoise_dct16(x, 0.15, **kw)}
+    fn = fns[case]
+    f32 = torch.float32
+    y = fn(out_dtype=f32)
+    yc = fn(out_dtype=f32, clamp=(0.1, 0.9))
+    assert torch.equal(yc, y.clamp(0.1, 0.9))
+    ys = fn(out_dtype=f32, scale=255.0, bias=-3.0)
+    assert torch.allclose(ys, y * 255.0 - 3.0, rtol=1e-6, atol=1e-4)
+    yb = fn(out_dtype=f32, scale=2.0, clamp=(0.0, 1.0))
+    assert torch.allclose(yb, (y * 2.0).clamp(0.0, 1.0), rtol=1e-6, atol=1e-6)
+    # bf16 output: the clamp on the rounded pair == round(clamp in f32)
+    for lo, hi in [(0.0, 1.0), (0.1, 0.9), (0.3337, 0.6663)]:
+        yh = fn(clamp=(lo, hi))
+        assert torch.equal(yh, y.clamp(lo, hi).bfloat16()), (lo, hi)
+    yh = fn(scale=2.0, bias=0.25, clamp=(0.0, 1.0))
+    assert torch.equal(yh, torch.addcmul(torch.full_like(y, 0.25), y, torch.full_like(y, 2.0))
+                       .clamp(0.0, 1.0).bfloat16())
+    # NaN propagates through the clamp (both output dtypes)
+    xn = x.clone()
+    xn[0, 100:140, 200:260] = float("nan")
+    fnn = {"fused": lambda **kw: pipelines.resample(xn, 272, 480, **kw),
+           "two_pass": lambda **kw: pipelines.resample(xn, 40, 70, **kw),
+           "gauss": lambda **kw: pipelines.gaussian_blur(xn, 9, **kw),
+           "dct": lambda **kw: pipelines.denoise_dct16(xn, 0.15, **kw)}[case]
+    for dt in (f32, torch.bfloat16):
+        a = fnn(out_dtype=dt)
+        b = fnn(out_dtype=dt, clamp=(0.0, 1.0))
+        assert torch.equal(torch.isnan(a), torch.isnan(b))
+        assert torch.isnan(b).any()
