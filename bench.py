@@ -41,7 +41,7 @@ CONFIGS = {
     "c2": (2160, 3840, 1080, 1920, "lanczos", 0,
            "c2: 4K (3840x2160) RGB bf16 -> 1080p, separable Lanczos-3 2x, fp32 accumulate, bf16 out"),
     "c1": (1080, 1920, 540, 960, "lanczos", 0,
-           "c1: 1080p RGB f32 -> 540p, separable Lanczos-3 2x (bf16 operands, fp32 accumulate), f32 out"),
+           "c1: 1080p RGB f32 -> 540p, separable Lanczos-3 2x, f32 throughout (FMA pipe, bit-exact to the reference), f32 out"),
     "c3-9": (4320, 7680, 4320, 7680, "gauss", 9, "c3: 8K RGB bf16 separable Gaussian, 9 taps"),
     "c3-15": (4320, 7680, 4320, 7680, "gauss", 15, "c3: 8K RGB bf16 separable Gaussian, 15 taps"),
     "c3-21": (4320, 7680, 4320, 7680, "gauss", 21, "c3: 8K RGB bf16 separable Gaussian, 21 taps"),
@@ -276,9 +276,10 @@ def run_b200(args):
         kernel_name = ("tsb::separable_kernel (fused V+H tcgen05 pass)" if fused else
                        "tsb::axis_pass_kernel x2 (vertical + horizontal, bf16 intermediate; "
                        "alg bytes exclude the intermediate)")
-        launches_per_step = (1 if fused else 2) + (1 if in_dtype == torch.float32 else 0)
-        if in_dtype == torch.float32:
-            kernel_name = "f32->bf16 cast kernel + " + kernel_name + " (timed together)"
+        launches_per_step = 1 if fused else 2
+        if in_dtype == torch.float32:  # pipelines._run_f32: one f32 kernel, no bf16 copy
+            kernel_name = "tsb::separable_f32_kernel<2,12,3> (f32 FMA-pipe fused H+V pass" + (", exact roundings)" if _pl.F32_EXACT else ")")
+            launches_per_step = 1
     alg_bytes = in_bytes + out_bytes  # per launch per GPU
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
@@ -324,7 +325,7 @@ def run_b200(args):
                     "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out_bytes,
                     "api": "paper_2512_02371_b200.pipelines.run_from_host (pinned host -> device -> "
                            "host, copies overlapped with kernels over 3 streams)"},
-            "gpu_launches": K * launches_per_step,  # incl. the f32->bf16 cast kernel (c1)
+            "gpu_launches": K * launches_per_step,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",

@@ -241,6 +241,29 @@ typedef struct ts_conv_group {
  * over a lowered conv group (interp.py:419-486, 488-534). */
 TS_API ts_status ts_run_conv_group(const ts_conv_group* group, void* stream);
 
+/* f32-input separable transform on the FMA pipe (config c1: an f32 image is
+ * read once, no bf16 copy).  Replaces, for f32 images, the two 1-D
+ * source-form conv passes of the reference (interp.py:162-167, 203-211;
+ * oracle/pipelines_ref.py:78-97) in their exact evaluation order —
+ * horizontal pass first, taps summed left to right, then + 0.  With
+ * flags & TS_F32_EXACT every product and sum is rounded separately, as the
+ * reference does, and f32 outputs are bit-identical to the reference's;
+ * without it each tap is one fused multiply-add (faster; differs from the
+ * reference by f32 rounding only, ~1e-7).  Uniform axes only: output o of an
+ * axis reads inputs clamp(stride*o + base + t), t < taps, with the SAME taps
+ * weights[t] for every o (device f32).  Instantiated (stride, taps, base & 3):
+ * (2, 12, 3) = Lanczos-3 2x, (1, 9|15|21|31, -(taps-1)/2 & 3) = centred
+ * filters; others return TS_ERR_UNSUPPORTED.  out: f32 or bf16 (strides in
+ * elements); ep may be NULL. */
+#define TS_F32_EXACT 0x1
+TS_API ts_status ts_separable_f32_ep(int planes, const float* in, int in_h, int in_w,
+                                     int64_t in_row_stride, int64_t in_plane_stride, int stride,
+                                     int taps, int row_base, const float* row_weights, int out_h,
+                                     int col_base, const float* col_weights, int out_w, void* out,
+                                     int64_t out_row_stride, int64_t out_plane_stride,
+                                     int out_dtype, int flags, const ts_epilogue* ep,
+                                     void* stream);
+
 /* Elementwise f32 -> bf16 (round to nearest even), n elements. */
 TS_API ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream);
 

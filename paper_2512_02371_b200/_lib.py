@@ -88,6 +88,8 @@ _SIGNATURES = {
     "ts_probe_m64": (_I, [_P, _P, _P, _I, _I, _P]),
     "ts_probe_issue2": (_I, [_I, _I, _I, _I, _I, _P, _P]),
     "ts_cast_f32_bf16": (_I, [_P, _P, _I64, _P]),
+    "ts_separable_f32_ep": (_I, [_I, _P, _I, _I, _I64, _I64, _I, _I, _I, _P, _I, _I, _P, _I, _P,
+                                 _I64, _I64, _I, _I, _P, _P]),
     "ts_run_conv_group": (_I, [_P, _P]),
     "ts_debug_dct16": (_I, [_P]),
     "ts_denoise_dct16": (_I, [_P, _I64, _I64, _I, _P, _I64, _I64, _I, _I, _I, _I,

@@ -37,6 +37,32 @@ class Axis:
         self.device = device
         self.n_in, self.n_out = int(n_in), int(n_out)
         self.info = self._info()
+        self.first, self.weights = first, weights  # f32 taps (the FMA-pipe f32 path)
+
+    @property
+    def uniform(self):
+        """(stride, taps, base) when output o reads inputs stride*o + base + t
+        with the same taps for every o (the f32 kernel's precondition), else
+        None."""
+        first = getattr(self, "first", None)
+        if first is None or self.n_out < 1:
+            return None
+        base = int(first[0])
+        stride = int(first[1] - first[0]) if self.n_out > 1 else 1
+        if stride < 1 or not np.array_equal(
+                first, base + stride * np.arange(self.n_out, dtype=np.int64)):
+            return None
+        if not (self.weights == self.weights[:1]).all():
+            return None
+        return stride, int(self.weights.shape[1]), base
+
+    def device_weights(self):
+        """The f32 taps as a device tensor (n_out x taps), uploaded once."""
+        w = getattr(self, "_wdev", None)
+        if w is None:
+            import torch
+            w = self._wdev = torch.from_numpy(self.weights).to(f"cuda:{self.device}")
+        return w
 
     @classmethod
     def from_toeplitz(cls, spec: layout.ToeplitzSpec, kernel, n_in: int, n_out: int,

@@ -1,0 +1,251 @@
+// separable_f32.cu — f32-input separable transform on the FMA pipe.
+//
+// Config c1 (a 1080p f32 image, Lanczos-3 2x) is HBM-bound at ~9 multiply-adds
+// per input pixel (2 FLOP per HBM byte, far below the FP32 pipe's ridge), so
+// the tensor-core path's separate f32 -> bf16 cast (4 B read + 2 B write +
+// 2 B re-read per pixel) costs more than the arithmetic it feeds.  This kernel
+// reads the f32 image once, keeps every intermediate in f32 and follows the
+// order of the reference's source-form conv statement (one 1-D pass per
+// axis, horizontal first, taps summed left to right, then `+ acc` with
+// acc = 0 — interp.py:162-167, 203-211; restated in
+// oracle/pipelines_ref.py:78-97); in TS_F32_EXACT mode its f32 output is
+// bit-identical to the oracle's.
+//
+// Uniform axes only (first[o] = S*o + base and the same T taps for every
+// output: the exact-2x Lanczos-3 axis and the centred filters): one CTA per
+// 32 x 64 output tile stages its (S*31+T) x (S*63+T) input window with
+// 16-byte cp.async (per-column clamped 4-byte copies at image edges — the
+// reference's clamp-to-edge), runs the horizontal pass into a shared f32
+// buffer, then the vertical pass straight to global.  Taps live in
+// registers; each thread computes 4 consecutive outputs from one register
+// window (float4 shared loads of S*3+T inputs instead of 4*T scalar ones);
+// the vertical pass takes column pairs through packed f32x2 FMAs (FFMA2).
+// With TS_F32_EXACT the taps are multiplied and added separately (the
+// reference's rounding, bit-exact); without it they are fused multiply-adds
+// (one rounding per tap fewer, ~half the FP32 instructions).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "sm100.cuh"
+
+namespace tsb {
+namespace {
+
+constexpr int kTR = 32, kTC = 64, kThreads = 256, kR = 4;
+
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// Window geometry of one tile for (stride S, taps T, column misalignment OFF):
+// the staged window starts at the 16-byte-aligned column c0 - OFF.
+template <int S, int T, int OFF>
+struct Geo {
+  static constexpr int SR = S * (kTR - 1) + T;             // window rows
+  static constexpr int SCA = (OFF + S * (kTC - 1) + T + 3) & ~3;  // aligned window columns
+  static constexpr int WP = ((SCA + 27) & ~31) + 4;        // pitch = 4 mod 32 floats: the
+                                                           // float4 row walks of 8 lanes
+                                                           // cover all 32 banks
+  static constexpr int HP = kTC + 4;                       // 4 mod 32: float4 stores of 8
+                                                           // lanes on consecutive rows and
+                                                           // float2 column-pair loads are
+                                                           // conflict-free
+  static constexpr int NV = S * (kR - 1) + T;              // taps of kR outputs
+  static constexpr int NVA = (OFF + NV + 3) & ~3;          // as whole float4s
+  static constexpr int smem = 4 * (SR * WP + SR * HP);
+};
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // FFMA2
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+template <int S, int T, int OFF, bool BF16, bool EXACT>
+__global__ void __launch_bounds__(kThreads, 3) separable_f32_kernel(
+    const float* __restrict__ in, int H, int W, int64_t irs, int64_t ips, int vec_ok,
+    void* __restrict__ out, int OH, int OW, int64_t ors, int64_t ops, int rbase, int cbase,
+    const float* __restrict__ rw, const float* __restrict__ cw, EpiK ek) {
+  using G = Geo<S, T, OFF>;
+  extern __shared__ __align__(16) float sm[];
+  float* win = sm;                  // SR x WP  input window (f32, as loaded)
+  float* hb = win + G::SR * G::WP;  // SR x HP  horizontal pass
+
+  const int p = blockIdx.z, or0 = blockIdx.y * kTR, oc0 = blockIdx.x * kTC;
+  const int r0 = S * or0 + rbase, c0a = S * oc0 + cbase - OFF;
+  const float* src = in + p * ips;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(win));
+  constexpr int QC = G::SCA / 4;  // 16-byte chunks per window row
+  for (int idx = tid; idx < G::SR * QC; idx += kThreads) {
+    const int r = idx / QC, q = idx - r * QC;
+    const float* row = src + static_cast<int64_t>(min(max(r0 + r, 0), H - 1)) * irs;
+    const int gc = c0a + 4 * q;
+    const uint32_t d = wbase + 4u * (r * G::WP + 4 * q);
+    if (vec_ok && gc >= 0 && gc + 3 < W) {
+      cp_async16(d, row + gc);
+    } else {  // image edge: clamp each column (the reference's clamp-to-edge)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cp_async4(d + 4u * e, row + min(max(gc + e, 0), W - 1));
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  // every output of a uniform axis has the same taps: hold them in registers
+  float wc[T];
+  float2 wr2[T];  // row taps duplicated for the packed column-pair FMAs
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    wc[t] = __ldg(cw + t);
+    const float w = __ldg(rw + t);
+    wr2[t] = make_float2(w, w);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+
+  // horizontal pass: task = (group g of kR output columns, window row r); the
+  // lanes of a warp walk consecutive rows
+  for (int task = tid; task < G::SR * (kTC / kR); task += kThreads) {
+    const int g = task / G::SR, r = task - g * G::SR;
+    const float4* x = reinterpret_cast<const float4*>(win + r * G::WP + S * kR * g);
+    float v[G::NVA];
+#pragma unroll
+    for (int i = 0; i < G::NVA / 4; ++i) {
+      const float4 f = x[i];
+      v[4 * i] = f.x, v[4 * i + 1] = f.y, v[4 * i + 2] = f.z, v[4 * i + 3] = f.w;
+    }
+    float o[kR];
+#pragma unroll
+    for (int k = 0; k < kR; ++k) {
+      float acc = __fmul_rn(v[OFF + S * k], wc[0]);
+#pragma unroll
+      for (int t = 1; t < T; ++t)
+        acc = EXACT ? __fadd_rn(acc, __fmul_rn(v[OFF + S * k + t], wc[t]))
+                    : fmaf(v[OFF + S * k + t], wc[t], acc);
+      o[k] = __fadd_rn(acc, 0.0f);
+    }
+    *reinterpret_cast<float4*>(hb + r * G::HP + kR * g) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+
+  // vertical pass: task = (group g of kR output rows, column pair j, j+1);
+  // the lanes walk consecutive column pairs (one float2 per window row), and
+  // the fast mode runs both columns through one packed FFMA2 per tap
+  for (int task = tid; task < (kTR / kR) * (kTC / 2); task += kThreads) {
+    const int g = task / (kTC / 2), j = 2 * (task - g * (kTC / 2));
+    const int oc = oc0 + j;
+    const float2* x = reinterpret_cast<const float2*>(hb + S * kR * g * G::HP + j);
+    float2 v[G::NV];
+#pragma unroll
+    for (int i = 0; i < G::NV; ++i) v[i] = x[i * (G::HP / 2)];
+#pragma unroll
+    for (int k = 0; k < kR; ++k) {
+      float2 acc = make_float2(__fmul_rn(v[S * k].x, wr2[0].x), __fmul_rn(v[S * k].y, wr2[0].x));
+#pragma unroll
+      for (int t = 1; t < T; ++t) {
+        if constexpr (EXACT) {
+          acc.x = __fadd_rn(acc.x, __fmul_rn(v[S * k + t].x, wr2[t].x));
+          acc.y = __fadd_rn(acc.y, __fmul_rn(v[S * k + t].y, wr2[t].x));
+        } else {
+          acc = ffma2(v[S * k + t], wr2[t], acc);
+        }
+      }
+      const int orow = or0 + kR * g + k;
+      if (orow < OH) {
+        const float y0 = epi_f32(ek, __fadd_rn(acc.x, 0.0f));
+        const float y1 = epi_f32(ek, __fadd_rn(acc.y, 0.0f));
+        const int64_t o = p * ops + orow * ors + oc;
+        if constexpr (BF16) {
+          if (oc < OW) static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(y0);
+          if (oc + 1 < OW) static_cast<__nv_bfloat16*>(out)[o + 1] = __float2bfloat16_rn(y1);
+        } else {
+          if (oc < OW) static_cast<float*>(out)[o] = y0;
+          if (oc + 1 < OW) static_cast<float*>(out)[o + 1] = y1;
+        }
+      }
+    }
+  }
+}
+
+template <int S, int T, int OFF, bool BF16, bool EXACT>
+ts_status launch_f32(int planes, const float* in, int H, int W, int64_t irs, int64_t ips, int rb,
+                     const float* rw, int OH, int cb, const float* cw, int OW, void* out,
+                     int64_t ors, int64_t ops, const EpiK& ek, cudaStream_t st) {
+  constexpr int smem = Geo<S, T, OFF>::smem;
+  auto fn = separable_f32_kernel<S, T, OFF, BF16, EXACT>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr != cudaSuccess) return cuda_error(attr, "separable_f32: smem attribute");
+  const int vec_ok = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && irs % 4 == 0 && ips % 4 == 0;
+  dim3 grid((OW + kTC - 1) / kTC, (OH + kTR - 1) / kTR, planes);
+  fn<<<grid, kThreads, smem, st>>>(in, H, W, irs, ips, vec_ok, out, OH, OW, ors, ops, rb, cb, rw,
+                                   cw, ek);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "separable_f32 launch");
+}
+
+template <int S, int T, int OFF>
+ts_status launch_f32_any(bool bf, bool exact, int planes, const float* in, int H, int W,
+                         int64_t irs, int64_t ips, int rb, const float* rw, int OH, int cb,
+                         const float* cw, int OW, void* out, int64_t ors, int64_t ops,
+                         const EpiK& ek, cudaStream_t st) {
+#define TS_F32_ARGS planes, in, H, W, irs, ips, rb, rw, OH, cb, cw, OW, out, ors, ops, ek, st
+  if (bf) return exact ? launch_f32<S, T, OFF, true, true>(TS_F32_ARGS)
+                       : launch_f32<S, T, OFF, true, false>(TS_F32_ARGS);
+  return exact ? launch_f32<S, T, OFF, false, true>(TS_F32_ARGS)
+               : launch_f32<S, T, OFF, false, false>(TS_F32_ARGS);
+#undef TS_F32_ARGS
+}
+
+}  // namespace
+}  // namespace tsb
+
+using namespace tsb;
+
+extern "C" ts_status ts_separable_f32_ep(int planes, const float* in, int in_h, int in_w,
+                                         int64_t in_row_stride, int64_t in_plane_stride,
+                                         int stride, int taps, int row_base,
+                                         const float* row_weights, int out_h, int col_base,
+                                         const float* col_weights, int out_w, void* out,
+                                         int64_t out_row_stride, int64_t out_plane_stride,
+                                         int out_dtype, int flags, const ts_epilogue* ep,
+                                         void* stream) {
+  if (planes < 0 || in_h < 1 || in_w < 1 || out_h < 1 || out_w < 1 || planes > 65535)
+    return set_error(TS_ERR_INVALID, "separable_f32: bad sizes");
+  if (planes == 0) return TS_OK;
+  if (!in || !out || !row_weights || !col_weights)
+    return set_error(TS_ERR_INVALID, "separable_f32: null pointer");
+  if (out_dtype != TS_F32 && out_dtype != TS_BF16)
+    return set_error(TS_ERR_INVALID, "separable_f32: out dtype must be f32 or bf16");
+  if (in_row_stride < in_w || in_plane_stride < in_row_stride * in_h ||
+      out_row_stride < out_w || out_plane_stride < out_row_stride * out_h)
+    return set_error(TS_ERR_INVALID, "separable_f32: strides smaller than the image");
+  if (ep && ep->lo > ep->hi) return set_error(TS_ERR_INVALID, "epilogue: lo > hi");
+  const EpiK ek = make_epik(ep);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool bf = out_dtype == TS_BF16, exact = flags & TS_F32_EXACT;
+  const int off = col_base & 3;  // misalignment of every tile's first column
+#define TS_F32_CASE(S_, T_, OFF_)                                                                \
+  if (stride == S_ && taps == T_ && off == OFF_)                                                 \
+    return launch_f32_any<S_, T_, OFF_>(bf, exact, planes, in, in_h, in_w, in_row_stride,        \
+                                        in_plane_stride, row_base, row_weights, out_h, col_base, \
+                                        col_weights, out_w, out, out_row_stride,                 \
+                                        out_plane_stride, ek, st);
+  TS_F32_CASE(2, 12, 3)  // Lanczos-3 2x: first tap 2o - 5
+  TS_F32_CASE(1, 9, 0)   // centred filters: first tap o - (T-1)/2
+  TS_F32_CASE(1, 15, 1)
+  TS_F32_CASE(1, 21, 2)
+  TS_F32_CASE(1, 31, 1)
+#undef TS_F32_CASE
+  return set_error(TS_ERR_UNSUPPORTED,
+                   "separable_f32: (stride %d, taps %d, column base %d) not instantiated", stride,
+                   taps, col_base);
+}

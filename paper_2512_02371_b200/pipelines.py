@@ -25,6 +25,7 @@ kernels without an epilogue run.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -109,6 +110,41 @@ def _ep_ptr(ep):
     return ctypes.byref(ep)
 
 
+# (stride, taps, base & 3) csrc/separable_f32.cu instantiates
+_F32_KERNELS = frozenset({(2, 12, 3), (1, 9, 0), (1, 15, 1), (1, 21, 2), (1, 31, 1)})
+
+# f32 images: True = the reference's separate product / sum roundings
+# (bit-identical f32 output, slower), False = one fused multiply-add per tap.
+# Default from TSB_F32_EXACT=1 in the environment.
+F32_EXACT = os.environ.get("TSB_F32_EXACT", "0") == "1"
+
+
+def _run_f32(x, ra, ca, out_dtype, ep, stream):
+    """f32 images through ``ts_separable_f32_ep`` (FMA pipe, the f32 image
+    read once; bit-identical to the reference's f32 evaluation when
+    ``F32_EXACT``) when
+    both axes are uniform-stride with an instantiated (stride, taps);
+    otherwise None and the caller takes the bf16 tensor-core path."""
+    ur, uc = ra.uniform, ca.uniform
+    if (ur is None or uc is None or ur[:2] != uc[:2]
+            or (uc[0], uc[1], uc[2] & 3) not in _F32_KERNELS):
+        return None
+    torch = _torch()
+    H, W = x.shape[-2], x.shape[-1]
+    P = math.prod(x.shape[:-2]) if x.dim() > 2 else 1
+    if P > 65535:
+        return None
+    oh, ow = ra.n_out, ca.n_out
+    out = torch.empty((P, oh, ow), dtype=out_dtype, device=x.device)
+    ts_out = _lib.TS_BF16 if out_dtype == torch.bfloat16 else _lib.TS_F32
+    wr, wc = ra.device_weights(), ca.device_weights()
+    _lib.check(_lib.load().ts_separable_f32_ep(
+        P, x.data_ptr(), H, W, W, W * H, ur[0], ur[1], ur[2], wr.data_ptr(), oh, uc[2],
+        wc.data_ptr(), ow, out.data_ptr(), ow, ow * oh, ts_out, 1 if F32_EXACT else 0,
+        None if ep is None else _ep_ptr(ep), stream), "ts_separable_f32_ep")
+    return out.reshape(*x.shape[:-2], oh, ow)
+
+
 def _run(x, ra, ca, out_dtype, ep=None):
     torch = _torch()
     _check_device(x)
@@ -121,6 +157,10 @@ def _run(x, ra, ca, out_dtype, ep=None):
     oh, ow = ra.n_out, ca.n_out
     if x.numel() == 0:  # empty batch: nothing to launch
         return torch.empty((*x.shape[:-2], oh, ow), dtype=out_dtype, device=x.device)
+    if x.dtype == torch.float32 and x.is_contiguous():
+        y = _run_f32(x, ra, ca, out_dtype, ep, stream)
+        if y is not None:
+            return y
     inb, in_rs = _as_planes_bf16(x, stream)
     P = inb.shape[0]
     align = 8 if out_dtype == torch.bfloat16 else 4

@@ -91,9 +91,11 @@ def test_f32_input_and_output():
     x = torch.rand((3, 1080, 1920), generator=g).cuda()
     y = pipelines.downsample2x(x)
     assert y.dtype == torch.float32 and y.shape == (3, 540, 960)
+    # f32 images take the f32 FMA-pipe kernel (test_gpu_separable_f32.py);
+    # the bf16 tensor-core path differs from it by bf16 operand rounding
     yb = pipelines.downsample2x(x.bfloat16(), out_dtype=torch.float32)
     torch.cuda.synchronize()
-    assert torch.equal(y, yb)
+    assert (y - yb).abs().max().item() <= 8e-3
 
 
 def _variant(ra, ca, planes=1, out_dtype=1):
