@@ -85,36 +85,46 @@ __global__ void __launch_bounds__(kThreads, 3) separable_f32_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(win));
+  // the window streams in as two cp.async groups (top / bottom rows): the
+  // horizontal pass over the top rows overlaps the bottom rows' loads
   constexpr int QC = G::SCA / 4;  // 16-byte chunks per window row
-  for (int idx = tid; idx < G::SR * QC; idx += kThreads) {
-    const int r = idx / QC, q = idx - r * QC;
-    const float* row = src + static_cast<int64_t>(min(max(r0 + r, 0), H - 1)) * irs;
-    const int gc = c0a + 4 * q;
-    const uint32_t d = wbase + 4u * (r * G::WP + 4 * q);
-    if (vec_ok && gc >= 0 && gc + 3 < W) {
-      cp_async16(d, row + gc);
-    } else {  // image edge: clamp each column (the reference's clamp-to-edge)
+  constexpr int RH = G::SR / 2;
+  auto stage = [&](int lo, int hi) {
+    for (int idx = lo * QC + tid; idx < hi * QC; idx += kThreads) {
+      const int r = idx / QC, q = idx - r * QC;
+      const float* row = src + static_cast<int64_t>(min(max(r0 + r, 0), H - 1)) * irs;
+      const int gc = c0a + 4 * q;
+      const uint32_t d = wbase + 4u * (r * G::WP + 4 * q);
+      if (vec_ok && gc >= 0 && gc + 3 < W) {
+        cp_async16(d, row + gc);
+      } else {  // image edge: clamp each column (the reference's clamp-to-edge)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) cp_async4(d + 4u * e, row + min(max(gc + e, 0), W - 1));
+        for (int e = 0; e < 4; ++e) cp_async4(d + 4u * e, row + min(max(gc + e, 0), W - 1));
+      }
     }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage(0, RH);
+  stage(RH, G::SR);
   // every output of a uniform axis has the same taps: hold them in registers
   float wc[T];
   float2 wr2[T];  // row taps duplicated for the packed column-pair FMAs
+  float2 wcp[T / 2];  // column taps (OFF & 1) + 2i, + 2i + 1 as register pairs (S == 2)
 #pragma unroll
   for (int t = 0; t < T; ++t) {
     wc[t] = __ldg(cw + t);
     const float w = __ldg(rw + t);
     wr2[t] = make_float2(w, w);
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < T / 2; ++i)
+    wcp[i] = make_float2(wc[min((OFF & 1) + 2 * i, T - 1)], wc[min((OFF & 1) + 2 * i + 1, T - 1)]);
 
   // horizontal pass: task = (group g of kR output columns, window row r); the
   // lanes of a warp walk consecutive rows
-  for (int task = tid; task < G::SR * (kTC / kR); task += kThreads) {
-    const int g = task / G::SR, r = task - g * G::SR;
+  auto hpass = [&](int lo, int hi) {
+  for (int task = tid; task < (hi - lo) * (kTC / kR); task += kThreads) {
+    const int g = task / (hi - lo), r = lo + task - g * (hi - lo);
     const float4* x = reinterpret_cast<const float4*>(win + r * G::WP + S * kR * g);
     float v[G::NVA];
 #pragma unroll
@@ -123,6 +133,25 @@ __global__ void __launch_bounds__(kThreads, 3) separable_f32_kernel(
       v[4 * i] = f.x, v[4 * i + 1] = f.y, v[4 * i + 2] = f.z, v[4 * i + 3] = f.w;
     }
     float o[kR];
+    if constexpr (!EXACT && S == 2) {
+      // even stride: input OFF + 2k + t sits at an even register index for
+      // every output k exactly when t = OFF (mod 2), so taps (t, t+1) from
+      // there on are one aligned register pair -> one FFMA2 per two taps
+      // (even- and odd-tap partial sums, added at the end)
+      constexpr int T0 = OFF & 1, NP = (T - T0) / 2;
+#pragma unroll
+      for (int k = 0; k < kR; ++k) {
+        const int e = OFF + S * k + T0;
+        float2 acc2 = make_float2(__fmul_rn(v[e], wcp[0].x), __fmul_rn(v[e + 1], wcp[0].y));
+#pragma unroll
+        for (int i = 1; i < NP; ++i) acc2 = ffma2(make_float2(v[e + 2 * i], v[e + 2 * i + 1]), wcp[i], acc2);
+#pragma unroll
+        for (int t = 0; t < T0; ++t) acc2.x = fmaf(v[OFF + S * k + t], wc[t], acc2.x);
+#pragma unroll
+        for (int t = T0 + 2 * NP; t < T; ++t) acc2.y = fmaf(v[OFF + S * k + t], wc[t], acc2.y);
+        o[k] = acc2.x + acc2.y;
+      }
+    } else {
 #pragma unroll
     for (int k = 0; k < kR; ++k) {
       float acc = __fmul_rn(v[OFF + S * k], wc[0]);
@@ -132,8 +161,16 @@ __global__ void __launch_bounds__(kThreads, 3) separable_f32_kernel(
                     : fmaf(v[OFF + S * k + t], wc[t], acc);
       o[k] = __fadd_rn(acc, 0.0f);
     }
+    }
     *reinterpret_cast<float4*>(hb + r * G::HP + kR * g) = make_float4(o[0], o[1], o[2], o[3]);
   }
+  };
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncthreads();
+  hpass(0, RH);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  hpass(RH, G::SR);
   __syncthreads();
 
   // vertical pass: task = (group g of kR output rows, column pair j, j+1);
