@@ -70,7 +70,7 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // FFMA
 }
 
 template <int S, int T, int OFF, bool BF16, bool EXACT>
-__global__ void __launch_bounds__(kThreads, 3) separable_f32_kernel(
+__global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel(
     const float* __restrict__ in, int H, int W, int64_t irs, int64_t ips, int vec_ok,
     void* __restrict__ out, int OH, int OW, int64_t ors, int64_t ops, int rbase, int cbase,
     const float* __restrict__ rw, const float* __restrict__ cw, EpiK ek) {
