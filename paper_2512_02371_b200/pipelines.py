@@ -10,8 +10,10 @@ fused sm_100a kernels behind the C ABI:
   same-size separable convolution (config 3).
 
 Images are planar: a tensor ``(..., H, W)`` is a stack of planes (RGB
-counts as 3 planes).  Inputs are bf16 (or f32, cast to bf16 on the device);
-accumulation is f32 on the tensor cores.  Edges are clamp-to-edge.  There is
+counts as 3 planes).  bf16 inputs run on the tensor cores (f32 accumulate);
+f32 inputs on uniform axes (exact-2x Lanczos-3, centred filters) run in f32
+on the FMA pipe (``ts_separable_f32_ep``; bit-identical to the reference
+with ``F32_EXACT``), other f32 inputs are cast to bf16 on the device.  Edges are clamp-to-edge.  There is
 no CPU path: without the native library or a CUDA device these raise.
 
 Every pipeline takes an optional output epilogue, applied inside the
@@ -154,6 +156,8 @@ def _run(x, ra, ca, out_dtype, ep=None):
         raise ValueError(f"axes expect {ra.n_in} x {ca.n_in}, image is {H} x {W}")
     out_dtype = out_dtype or (x.dtype if x.dtype in (torch.bfloat16, torch.float32)
                               else torch.bfloat16)
+    if out_dtype not in (torch.bfloat16, torch.float32):
+        raise TypeError(f"unsupported out_dtype {out_dtype} (bf16 or f32)")
     oh, ow = ra.n_out, ca.n_out
     if x.numel() == 0:  # empty batch: nothing to launch
         return torch.empty((*x.shape[:-2], oh, ow), dtype=out_dtype, device=x.device)
@@ -270,6 +274,8 @@ def denoise_dct16(x, threshold: float = 0.15, mode: str = "hard", *, out_dtype=N
     H, W = x.shape[-2], x.shape[-1]
     out_dtype = out_dtype or (x.dtype if x.dtype in (torch.bfloat16, torch.float32)
                               else torch.bfloat16)
+    if out_dtype not in (torch.bfloat16, torch.float32):
+        raise TypeError(f"unsupported out_dtype {out_dtype} (bf16 or f32)")
     if x.numel() == 0:
         return torch.empty(x.shape, dtype=out_dtype, device=x.device)
     inb, in_rs = _as_planes_bf16(x, stream)

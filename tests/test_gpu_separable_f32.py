@@ -119,3 +119,14 @@ def test_f32_kernel_is_the_one_launched():
     rb = axis.lanczos3(64, 27, dev)
     if rb.uniform is None:
         assert pipelines._run_f32(x, rb, ca, torch.float32, None, pipelines._stream(x)) is None
+
+
+@pytest.mark.gpu
+def test_unsupported_out_dtype_raises():
+    """An out dtype the kernels cannot write is rejected before any launch."""
+    torch = _torch()
+    from paper_2512_02371_b200 import pipelines
+    for x in (torch.rand((1, 64, 128), device="cuda"),
+              torch.rand((1, 64, 128), device="cuda").bfloat16()):
+        with pytest.raises(TypeError):
+            pipelines.downsample2x(x, out_dtype=torch.float16)
