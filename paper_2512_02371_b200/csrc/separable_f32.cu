@@ -32,7 +32,7 @@
 namespace tsb {
 namespace {
 
-constexpr int kTR = 32, kTC = 64, kThreads = 256, kR = 4;
+constexpr int kTR = 32, kTC = 64, kThreads = 256, kR = 4, kRH = 8;
 
 __device__ __forceinline__ void cp_async4(uint32_t dst, const float* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
@@ -55,7 +55,8 @@ struct Geo {
                                                            // float2 column-pair loads are
                                                            // conflict-free
   static constexpr int NV = S * (kR - 1) + T;              // taps of kR outputs
-  static constexpr int NVA = (OFF + NV + 3) & ~3;          // as whole float4s
+  static constexpr int NVH = S * (kRH - 1) + T;            // taps of kRH horizontal outputs
+  static constexpr int NVA = (OFF + NVH + 3) & ~3;         // as whole float4s
   static constexpr int smem = 4 * (SR * WP + SR * HP);
 };
 
@@ -120,19 +121,19 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
   for (int i = 0; i < T / 2; ++i)
     wcp[i] = make_float2(wc[min((OFF & 1) + 2 * i, T - 1)], wc[min((OFF & 1) + 2 * i + 1, T - 1)]);
 
-  // horizontal pass: task = (group g of kR output columns, window row r); the
+  // horizontal pass: task = (group g of kRH output columns, window row r); the
   // lanes of a warp walk consecutive rows
   auto hpass = [&](int lo, int hi) {
-  for (int task = tid; task < (hi - lo) * (kTC / kR); task += kThreads) {
+  for (int task = tid; task < (hi - lo) * (kTC / kRH); task += kThreads) {
     const int g = task / (hi - lo), r = lo + task - g * (hi - lo);
-    const float4* x = reinterpret_cast<const float4*>(win + r * G::WP + S * kR * g);
+    const float4* x = reinterpret_cast<const float4*>(win + r * G::WP + S * kRH * g);
     float v[G::NVA];
 #pragma unroll
     for (int i = 0; i < G::NVA / 4; ++i) {
       const float4 f = x[i];
       v[4 * i] = f.x, v[4 * i + 1] = f.y, v[4 * i + 2] = f.z, v[4 * i + 3] = f.w;
     }
-    float o[kR];
+    float o[kRH];
     if constexpr (!EXACT && S == 2) {
       // even stride: input OFF + 2k + t sits at an even register index for
       // every output k exactly when t = OFF (mod 2), so taps (t, t+1) from
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
       // (even- and odd-tap partial sums, added at the end)
       constexpr int T0 = OFF & 1, NP = (T - T0) / 2;
 #pragma unroll
-      for (int k = 0; k < kR; ++k) {
+      for (int k = 0; k < kRH; ++k) {
         const int e = OFF + S * k + T0;
         float2 acc2 = make_float2(__fmul_rn(v[e], wcp[0].x), __fmul_rn(v[e + 1], wcp[0].y));
 #pragma unroll
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
       }
     } else {
 #pragma unroll
-    for (int k = 0; k < kR; ++k) {
+    for (int k = 0; k < kRH; ++k) {
       float acc = __fmul_rn(v[OFF + S * k], wc[0]);
 #pragma unroll
       for (int t = 1; t < T; ++t)
@@ -162,7 +163,10 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
       o[k] = __fadd_rn(acc, 0.0f);
     }
     }
-    *reinterpret_cast<float4*>(hb + r * G::HP + kR * g) = make_float4(o[0], o[1], o[2], o[3]);
+    #pragma unroll
+    for (int i = 0; i < kRH / 4; ++i)
+      *reinterpret_cast<float4*>(hb + r * G::HP + kRH * g + 4 * i) =
+          make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
   }
   };
   asm volatile("cp.async.wait_group 1;" ::: "memory");
