@@ -234,6 +234,8 @@ typedef struct ts_conv_group {
    * override a_base/a_stride/k_base/b_off. */
   const int32_t* a_idx;
   const int32_t* b_idx;
+  /* device int32[3], zeroed by the caller: on an out-of-bounds read the
+   * first failing thread writes {1 (src) | 2 (kern), index, iteration}. */
   int32_t* error;
 } ts_conv_group;
 

@@ -27,6 +27,16 @@ __device__ __forceinline__ float round_kind(float x, int kind) {
   return x;
 }
 
+// First out-of-bounds read wins: error[0] = 1 (src) | 2 (kern), error[1] =
+// the offending index, error[2] = the iteration (statement instance).
+__device__ __forceinline__ void report_oob(int32_t* error, int which, int index, int iteration) {
+  if (atomicCAS(error, 0, which) == 0) {
+    error[1] = index;
+    error[2] = iteration;
+    __threadfence();
+  }
+}
+
 __global__ void conv_group_kernel(ts_conv_group g) {
   const int64_t outs = static_cast<int64_t>(g.m) * g.n;
   const int64_t total = static_cast<int64_t>(g.instances) * outs;
@@ -48,7 +58,7 @@ __global__ void conv_group_kernel(ts_conv_group g) {
       for (int kk = 0; kk < g.k; ++kk) {
         const int ai = expl ? g.a_idx[xo + kk] : ab + kk;
         if (ai < 0 || ai >= g.src_len) {
-          atomicExch(g.error, 1 + ai);  // OutOfBounds on the A buffer
+          report_oob(g.error, 1, ai, v);  // OutOfBounds on the A buffer
           return;
         }
         const float a = round_kind(I[ai], g.src_kind);
@@ -57,7 +67,7 @@ __global__ void conv_group_kernel(ts_conv_group g) {
         if (off >= 0) {
           const int ki = kb + off;
           if (ki < 0 || ki >= g.kern_len) {
-            atomicExch(g.error, -(1 + ki));  // OutOfBounds on the kernel buffer
+            report_oob(g.error, 2, ki, v);  // OutOfBounds on the kernel buffer
             return;
           }
           b = round_kind(K[ki], g.kern_kind);

@@ -8,44 +8,57 @@ as ``ts_status`` codes which :func:`from_status` maps back.
 
 from __future__ import annotations
 
+# Interoperability with the reference: when the reference package is
+# importable next to this one (the drop-in case), every class below also
+# derives from its reference counterpart, so a caller's
+# ``except tensorsel.interp.OutOfBounds`` catches this package's errors too.
+try:  # pragma: no cover - depends on the caller's environment
+    from tensorsel import interp as _ref_interp, layout as _ref_layout
+except Exception:  # the reference is optional
+    _ref_interp = _ref_layout = None
 
-class EvalError(Exception):
+
+def _ref(mod, name):
+    return (getattr(mod, name),) if mod is not None and hasattr(mod, name) else ()
+
+
+class EvalError(*_ref(_ref_interp, "EvalError"), Exception):
     """interp.EvalError (interp.py:32)."""
 
 
-class OutOfBounds(EvalError):
+class OutOfBounds(EvalError, *_ref(_ref_interp, "OutOfBounds")):
     """interp.OutOfBounds (interp.py:36-39)."""
 
     def __init__(self, buffer, index=None):
         if index is None:  # message-only form from the native layer
-            super().__init__(buffer)
+            Exception.__init__(self, buffer)
             self.buffer, self.index = None, None
         else:
-            super().__init__(f"buffer {buffer!r} index {index} out of bounds")
+            Exception.__init__(self, f"buffer {buffer!r} index {index} out of bounds")
             self.buffer, self.index = buffer, index
 
 
-class DivideByZero(EvalError):
+class DivideByZero(EvalError, *_ref(_ref_interp, "DivideByZero")):
     """interp.DivideByZero (interp.py:42)."""
 
 
-class UnknownIntrinsic(EvalError):
+class UnknownIntrinsic(EvalError, *_ref(_ref_interp, "UnknownIntrinsic")):
     """interp.UnknownIntrinsic (interp.py:46)."""
 
 
-class ShapeUnregistered(EvalError):
+class ShapeUnregistered(EvalError, *_ref(_ref_interp, "ShapeUnregistered")):
     """interp.ShapeUnregistered (interp.py:50)."""
 
 
-class I32Overflow(EvalError):
+class I32Overflow(EvalError, *_ref(_ref_interp, "I32Overflow")):
     """interp.I32Overflow (interp.py:54)."""
 
 
-class PhaseMismatch(Exception):
+class PhaseMismatch(*_ref(_ref_layout, "PhaseMismatch"), Exception):
     """layout.PhaseMismatch (layout.py:24)."""
 
 
-class LayoutOutOfBounds(Exception):
+class LayoutOutOfBounds(*_ref(_ref_layout, "OutOfBounds"), Exception):
     """layout.OutOfBounds (layout.py:28)."""
 
 

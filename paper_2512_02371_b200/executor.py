@@ -24,12 +24,12 @@ there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
-import math
 
 import numpy as np
 
 from . import _lib, layout
-from .errors import EvalError, OutOfBounds, ShapeUnregistered, UnknownIntrinsic
+from .errors import (DivideByZero, EvalError, I32Overflow, OutOfBounds, ShapeUnregistered,
+                     UnknownIntrinsic)
 
 HARDWARE_SHAPES = (("wmma", 32, 16, 8), ("wmma", 16, 16, 16), ("amx", 16, 32, 16))
 _KIND = {"f32": 0, "f16": 1, "bf16": 2}
@@ -39,18 +39,20 @@ class UnsupportedProgram(EvalError):
     """A statement outside the conv family the GPU executor implements."""
 
 
-class Buffer:
-    """interp.Buffer (interp.py:132-136)."""
+try:  # the drop-in case: return the reference's own Buffer / BufferStore types
+    from tensorsel.interp import Buffer, BufferStore  # noqa: F401
+except Exception:  # reference not installed (e.g. on the GPU box): same-shaped mirrors
+    class Buffer:
+        """interp.Buffer (interp.py:132-136)."""
 
-    def __init__(self, kind, location, data):
-        self.kind, self.location, self.data = kind, location, data
+        def __init__(self, kind, location, data):
+            self.kind, self.location, self.data = kind, location, data
 
-    def __repr__(self):
-        return f"Buffer({self.kind!r}, {self.location!r}, <{len(self.data)}>)"
+        def __repr__(self):
+            return f"Buffer({self.kind!r}, {self.location!r}, <{len(self.data)}>)"
 
-
-class BufferStore(dict):
-    """interp.BufferStore: name -> Buffer."""
+    class BufferStore(dict):
+        """interp.BufferStore (interp.py:139-140): name -> Buffer."""
 
 
 def _cls(x):
@@ -58,27 +60,46 @@ def _cls(x):
 
 
 # ------------------------------------------------------------------ expressions
+def _check_i32(v):
+    """interp._check_i32 (interp.py:156-159)."""
+    if v >= 2 ** 31 or v < -(2 ** 31):
+        raise I32Overflow(f"i32 range exceeded (max {v}, min {v})")
+    return v
+
+
+def _check_i32_vec(a):
+    if a.size and (a.max() >= 2 ** 31 or a.min() < -(2 ** 31)):
+        raise I32Overflow(f"i32 range exceeded (max {a.max()}, min {a.min()})")
+    return a
+
+
+def _int_bop(op, a, b):
+    """interp._bop on i32 (interp.py:251-266): Euclidean / and %, overflow-checked."""
+    if op == "+":
+        return a + b
+    if op == "-":
+        return a - b
+    if op == "*":
+        return a * b
+    if op in ("/", "%"):
+        if np.any(np.asarray(b) == 0):
+            raise DivideByZero(f"integer {op} by zero")
+        r = np.mod(a, np.abs(b))
+        return r if op == "%" else (a - r) // b
+    raise EvalError(f"unknown op {op}")
+
+
 def _eval_int(e, env):
     c = _cls(e)
     if c == "Imm":
-        return int(e.value)
+        return _check_i32(int(e.value))
     if c == "Var":
         if e.name not in env:
             raise EvalError(f"unbound variable {e.name!r}")
         return env[e.name]
     if c == "Bop":
         a, b = _eval_int(e.lhs, env), _eval_int(e.rhs, env)
-        if e.op == "+":
-            return a + b
-        if e.op == "-":
-            return a - b
-        if e.op == "*":
-            return a * b
-        if e.op in ("/", "%"):
-            if b == 0:
-                raise EvalError("integer division by zero")
-            r = a % abs(b)
-            return r if e.op == "%" else (a - r) // b
+        return _check_i32(int(_int_bop(e.op, a, b)))
     raise UnsupportedProgram(f"non-scalar integer expression {c}")
 
 
@@ -86,15 +107,16 @@ def _eval_index(e, env):
     """Index vector of a Ramp/Broadcast tree (interp.py:191-202)."""
     c = _cls(e)
     if c in ("Imm", "Var", "Bop"):
-        if c == "Bop" and _cls(e.lhs) in ("Ramp", "Broadcast"):
+        if c == "Bop" and (_cls(e.lhs) in ("Ramp", "Broadcast")
+                           or _cls(e.rhs) in ("Ramp", "Broadcast")):
             a, b = _eval_index(e.lhs, env), _eval_index(e.rhs, env)
-            return {"+": a + b, "-": a - b, "*": a * b}[e.op]
+            return _check_i32_vec(_int_bop(e.op, a, b))
         return np.array([_eval_int(e, env)], np.int64)
     if c == "Ramp":
         base = _eval_index(e.base, env)
         stride = _eval_index(e.stride, env)
         steps = np.arange(e.steps).reshape(-1, 1)
-        return (base + steps * stride).reshape(-1)
+        return _check_i32_vec((base + steps * stride).reshape(-1))
     if c == "Broadcast":
         return np.tile(_eval_index(e.operand, env), e.copies)
     raise UnsupportedProgram(f"index expression {c}")
@@ -123,6 +145,7 @@ class _Group:
         self.b_off = None
         self.a_idx, self.b_idx = [], []   # explicit mode (source form)
         self.tmp = None                    # lowered: the temporary holding B
+        self.paths = []                    # statement path of every iteration
 
 
 class _Plan:
@@ -165,16 +188,56 @@ def _matrix_offsets(call, env):
     raise UnsupportedProgram(f"not a weight builder: {c} {getattr(call, 'name', '')}")
 
 
+def _annotate(err, sp):
+    """interp._exec_stmts's error annotation (interp.py:615-619): the first
+    (innermost) statement path is prefixed to the message."""
+    if not getattr(err, "stmt_path", None):
+        err.stmt_path = sp
+        err.args = (f"{sp}: {err.args[0]}",) if err.args else (sp,)
+    return err
+
+
+def _first_oob(idx, length):
+    bad = idx[(idx < 0) | (idx >= length)]
+    return int(bad.reshape(-1)[0]) if bad.size else None
+
+
 def _compile(p, extra_shapes, strict):
+    """Walk the program like interp._exec_stmts (interp.py:591-619) and
+    record its statements as plan ops.  Every index a conv-family program
+    touches is affine in the loop variables, so bounds are checked here, on
+    the host, in the reference's evaluation order; errors carry the
+    reference's statement path (``body[i][j]``)."""
     shapes = _shape_registry(p, extra_shapes, strict)
     kinds = {prm.name: prm.kind for prm in p.params}
+    lengths = {prm.name: prm.length for prm in p.params}
     plan = _Plan()
     tmp_defs = {}  # temporary name -> (kernel buf, base, offsets) of the current iteration
 
-    def emit_stmt(s, env, group_ctx):
+    def need(name):
+        if name not in lengths:
+            raise EvalError(f"unknown buffer {name!r}")
+        return lengths[name]
+
+    def check_range(name, lo, hi):
+        """A gather/scatter of indices [lo, hi] into `name` (interp._gather / _scatter)."""
+        n = need(name)
+        if lo < 0:
+            raise OutOfBounds(name, int(lo))
+        if hi >= n:
+            raise OutOfBounds(name, int(hi) if lo >= n else n)
+
+    def emit_stmt(s, env, sp):
+        try:
+            emit_one(s, env, sp)
+        except EvalError as err:
+            raise _annotate(err, sp)
+
+    def emit_one(s, env, sp):
         c = _cls(s)
         if c == "Allocate":
             kinds[s.name] = s.kind
+            lengths[s.name] = s.length
             plan.ops.append(("alloc", s.name, s.kind, s.length, s.location))
             return
         if c == "Evaluate":
@@ -187,15 +250,22 @@ def _compile(p, extra_shapes, strict):
                 tile = v.args[4]
                 if _cls(tile) != "Load" or not _is_flat(tile.index):
                     raise UnsupportedProgram("wmma_store of a non-buffer tile")
-                plan.ops.append(("store", out, tile.buffer, base, stride, cols, tile.index.steps))
+                lanes = tile.index.steps
+                check_range(tile.buffer, 0, lanes - 1)
+                rows = lanes // cols
+                idx = base + stride * np.arange(rows)[:, None] + np.arange(cols)[None, :]
+                bad = _first_oob(idx, need(out))
+                if bad is not None:
+                    raise OutOfBounds(out, bad)
+                plan.ops.append(("store", out, tile.buffer, idx.reshape(-1), lanes, sp))
                 return
             raise UnsupportedProgram(f"evaluate of {getattr(v, 'name', _cls(v))}")
         if c == "For":
             for it in range(s.min, s.min + s.extent):
                 env2 = dict(env)
                 env2[s.var] = it
-                for b in s.body:
-                    emit_stmt(b, env2, group_ctx)
+                for j, b in enumerate(s.body):
+                    emit_stmt(b, env2, f"{sp}[{j}]")
             return
         if c != "Store":
             raise UnsupportedProgram(f"statement {c}")
@@ -203,13 +273,23 @@ def _compile(p, extra_shapes, strict):
         vc = _cls(v)
         # acc = wmma_zero(m, n)
         if vc == "Call" and v.name == "wmma_zero":
-            plan.ops.append(("zero", s.buffer))
+            lanes = int(v.args[0].value) * int(v.args[1].value)
+            if not _is_flat(s.index, lanes):
+                raise UnsupportedProgram("wmma_zero must fill its accumulator from 0")
+            check_range(s.buffer, 0, lanes - 1)
+            plan.ops.append(("zero", s.buffer, lanes))
             return
         # tmp = weight builder
         if (vc == "Call" and v.name in ("ConvolutionShuffle", "PolyphaseShuffle")) or vc == "Shuffle":
             # recorded, not executed: the group that consumes it gathers B
             # on the fly, and materialises the last iteration's temporary
             kbuf, base, off, _ = _matrix_offsets(v, env)
+            used = off[off >= 0]
+            if used.size:  # the kernel window read (interp.py:488-534, 220-225)
+                check_range(kbuf, base + int(used.min()), base + int(used.max()))
+            if not _is_flat(s.index, len(off)):
+                raise UnsupportedProgram("weight temporary must be stored from 0")
+            check_range(s.buffer, 0, len(off) - 1)
             tmp_defs[s.buffer] = (kbuf, base, off)
             return
         # acc = wmma_mma(load_a, load_b, acc)
@@ -224,24 +304,33 @@ def _compile(p, extra_shapes, strict):
             tmp = lb.args[0].name
             b_base, b_stride = _eval_int(lb.args[1], env), _eval_int(lb.args[2], env)
             bk, bn = int(lb.args[3].value), int(lb.args[4].value)
+            # operand A: src[a_base + i*a_stride + kk] (interp._tile_gather, interp.py:408-410)
+            rows_off = a_stride * np.arange(m)
+            check_range(src, a_base + int(rows_off.min()), a_base + int(rows_off.max()) + k - 1)
             if bk != k or b_base != 0 or b_stride != bn:
                 raise UnsupportedProgram("wmma_load_b must read the whole temporary row-major")
-            if ("wmma", m, k, bn) not in shapes:
-                raise ShapeUnregistered(f"wmma_mma: shape wmma {m}x{k}x{bn} not registered")
             if tmp not in tmp_defs:
                 raise UnsupportedProgram(f"B operand {tmp!r} is not a weight temporary")
+            check_range(tmp, 0, k * bn - 1)
             kbuf, kb, off = tmp_defs[tmp]
             if len(off) != k * bn:
                 raise EvalError(f"temporary {tmp!r} has {len(off)} lanes, B needs {k * bn}")
-            if _cls(lc) == "Load" and lc.buffer == s.buffer and _is_flat(lc.index):
-                pass
+            if _cls(lc) == "Load" and lc.buffer == s.buffer and _is_flat(lc.index, m * bn):
+                check_range(s.buffer, 0, m * bn - 1)
             elif _cls(lc) == "Call" and lc.name == "wmma_zero":
-                plan.ops.append(("zero", s.buffer))
+                plan.ops.append(("zero", s.buffer, m * bn))
             else:
                 raise UnsupportedProgram("wmma_mma accumulator must be the stored buffer")
+            if ("wmma", m, k, bn) not in shapes:
+                raise ShapeUnregistered(f"wmma_mma: shape wmma {m}x{k}x{bn} not registered")
+            if not _is_flat(s.index):
+                raise UnsupportedProgram("wmma_mma result must be stored from 0")
+            if s.index.steps != m * bn:
+                raise EvalError(f"store index {s.index.steps} lanes, value {m * bn}")
+            check_range(s.buffer, 0, m * bn - 1)
             key = ("lowered", s.buffer, src, kbuf, m, k, bn, a_stride, off.tobytes())
             _append_iteration(plan, key, s.buffer, src, kbuf, m, k, bn, a_stride, a_base, kb, off,
-                              tmp)
+                              tmp, sp)
             return
         # acc = VectorReduceAdd(Load I * Load K) + Load acc  (source form)
         if vc == "Bop" and v.op == "+":
@@ -249,30 +338,37 @@ def _compile(p, extra_shapes, strict):
             if _cls(red) != "VectorReduceAdd":
                 red, acc = acc, red
             if _cls(red) == "VectorReduceAdd" and _cls(acc) == "Load" and acc.buffer == s.buffer:
-                _source_conv(plan, s, red, env, kinds)
+                _source_conv(plan, s, red, acc, env, check_range, sp)
                 return
         # dst = Load src (flat copy)
         if vc == "Load" and _is_flat(s.index) and _is_flat(v.index, s.index.steps):
-            plan.ops.append(("copy", s.buffer, v.buffer, s.index.steps, 0, 0))
+            n = s.index.steps
+            check_range(v.buffer, 0, n - 1)
+            check_range(s.buffer, 0, n - 1)
+            plan.ops.append(("copy", s.buffer, v.buffer, n, 0, 0))
             return
         # dst[ramp(bd, 1, n)] = Load src[ramp(bs, 1, n)]: a window copy at affine
         # offsets (e.g. each For iteration's accumulator into its output slot)
         if vc == "Load" and _unit_ramp(s.index) and _unit_ramp(v.index) \
                 and v.index.steps == s.index.steps:
-            plan.ops.append(("copy", s.buffer, v.buffer, s.index.steps,
-                             _eval_int(s.index.base, env), _eval_int(v.index.base, env)))
+            n = s.index.steps
+            bd, bs = _eval_int(s.index.base, env), _eval_int(v.index.base, env)
+            check_range(v.buffer, bs, bs + n - 1)
+            check_range(s.buffer, bd, bd + n - 1)
+            plan.ops.append(("copy", s.buffer, v.buffer, n, bd, bs))
             return
         if vc == "Broadcast" and _cls(v.operand) == "Imm" and _is_flat(s.index):
+            check_range(s.buffer, 0, s.index.steps - 1)
             plan.ops.append(("fill", s.buffer, float(v.operand.value), s.index.steps))
             return
         raise UnsupportedProgram(f"store into {s.buffer!r} of {vc} {getattr(v, 'name', '')}")
 
-    for st in p.body:
-        emit_stmt(st, {}, None)
+    for i, st in enumerate(p.body):
+        emit_stmt(st, {}, f"body[{i}]")
     return plan
 
 
-def _append_iteration(plan, key, acc, src, kbuf, m, k, n, a_stride, a_base, k_base, off, tmp):
+def _append_iteration(plan, key, acc, src, kbuf, m, k, n, a_stride, a_base, k_base, off, tmp, sp):
     last = plan.ops[-1] if plan.ops else None
     if last is not None and last[0] == "group" and last[1] == key:
         g = last[2]
@@ -282,17 +378,23 @@ def _append_iteration(plan, key, acc, src, kbuf, m, k, n, a_stride, a_base, k_ba
         plan.ops.append(("group", key, g))
     g.a_base.append(a_base)
     g.k_base.append(k_base)
+    g.paths.append(sp)
 
 
 def _strip_cast(e):
+    """Drop Cast-to-f32 nodes: on values already rounded to their buffer kind
+    they are the identity (interp._cast, interp.py:241-248).  A cast to any
+    other kind rounds or truncates, which the conv kernel does not model."""
     while _cls(e) == "Cast":
+        if e.vtype.kind != "f32":
+            raise UnsupportedProgram(f"cast to {e.vtype.kind} inside a conv statement")
         e = e.operand
     return e
 
 
-def _source_conv(plan, s, red, env, kinds):
+def _source_conv(plan, s, red, acc, env, check_range, sp):
     """VectorReduceAdd(n_out, Cast(Load I) * [Broadcast](Cast(Load K))) + acc."""
-    prod = red.operand
+    prod = _strip_cast(red.operand)
     if _cls(prod) != "Bop" or prod.op != "*":
         raise UnsupportedProgram("reduction operand must be a product")
     loads = []
@@ -302,18 +404,27 @@ def _source_conv(plan, s, red, env, kinds):
             e2 = _strip_cast(e.operand)
             if _cls(e2) != "Load":
                 raise UnsupportedProgram("broadcast of a non-load")
-            loads.append((e2.buffer, np.tile(_eval_index(e2.index, env), e.copies)))
+            ix = _eval_index(e2.index, env)
+            loads.append((e2.buffer, ix, np.tile(ix, e.copies)))
         elif _cls(e) == "Load":
-            loads.append((e.buffer, _eval_index(e.index, env)))
+            ix = _eval_index(e.index, env)
+            loads.append((e.buffer, ix, ix))
         else:
             raise UnsupportedProgram("product of non-loads")
-    (ib, ia), (kb, ka) = loads
+    for buf, ix, _ in loads:  # gathers in evaluation order (interp.py:183-185)
+        if ix.size:
+            check_range(buf, int(ix.min()), int(ix.max()))
+    (ib, _, ia), (kb, _, ka) = loads
     n_out = red.result_lanes
     if len(ia) != len(ka) or len(ia) % n_out:
         raise EvalError(f"cannot reduce {len(ia)} lanes to {n_out}")
     taps = len(ia) // n_out
+    if not _is_flat(acc.index, n_out):
+        raise UnsupportedProgram("source-form accumulator must be a flat load of its outputs")
+    check_range(acc.buffer, 0, n_out - 1)
     if not _is_flat(s.index, n_out):
         raise UnsupportedProgram("source-form store must be a flat ramp")
+    check_range(s.buffer, 0, n_out - 1)
     key = ("source", s.buffer, ib, kb, n_out, taps)
     last = plan.ops[-1] if plan.ops else None
     if last is not None and last[0] == "group" and last[1] == key:
@@ -325,6 +436,7 @@ def _source_conv(plan, s, red, env, kinds):
     g.b_idx.append(ka.reshape(n_out, taps).astype(np.int32))
     g.a_base.append(0)
     g.k_base.append(0)
+    g.paths.append(sp)
 
 
 # ------------------------------------------------------------------ execution
@@ -361,7 +473,7 @@ def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=N
                                           np.zeros((0, prm.length), np.float32)).to(dev)
         meta[prm.name] = (prm.kind, getattr(prm, "location", "mem"))
     stream = torch.cuda.current_stream(dev).cuda_stream
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    err = torch.zeros(3, dtype=torch.int32, device=dev)
     for op in plan.ops:
         kind = op[0]
         if kind == "alloc":
@@ -371,7 +483,7 @@ def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=N
             bufs[name] = torch.zeros((T, length), dtype=torch.float32, device=dev)
             meta[name] = (k, loc)
         elif kind == "zero":
-            bufs[op[1]].zero_()
+            bufs[op[1]][:, :op[2]] = 0
         elif kind == "fill":
             _, name, val, n = op
             bufs[name][:, :n] = val
@@ -390,12 +502,19 @@ def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=N
             vals = K[:, (base + o).clamp(min=0)]
             bufs[name][:, :len(off)] = torch.where(o >= 0, vals, torch.zeros_like(vals))
         elif kind == "store":
-            _, out, tile, base, stride, cols, lanes = op
-            rows = lanes // cols
-            idx = base + stride * np.arange(rows)[:, None] + np.arange(cols)[None, :]
-            if idx.min() < 0 or idx.max() >= bufs[out].shape[1]:
-                raise OutOfBounds(out, int(idx[(idx < 0) | (idx >= bufs[out].shape[1])][0]))
-            bufs[out][:, torch.from_numpy(idx.reshape(-1)).to(dev)] = bufs[tile][:, :lanes]
+            _, out, tile, idx, lanes, _sp = op
+            pos = np.arange(lanes)
+            if len(np.unique(idx)) != len(idx):
+                # interp._scatter (interp.py:549-553): colliding lanes, last wins + a lint
+                if lint_sink is not None:
+                    lint_sink.extend([f"store into {out!r} has colliding lanes (last wins)"] * T)
+                last = {}
+                for q, i in enumerate(idx.tolist()):
+                    last[i] = q
+                pos = np.fromiter(last.values(), np.int64)
+                idx = np.fromiter(last.keys(), np.int64)
+            src_pos = torch.from_numpy(pos).to(dev)
+            bufs[out][:, torch.from_numpy(idx).to(dev)] = bufs[tile][:, src_pos]
         elif kind == "group":
             _run_group(lib, op[2], bufs, meta, T, dev, stream, err)
         else:
@@ -443,11 +562,10 @@ def _run_group(lib, g, bufs, meta, T, dev, stream, err):
     err.zero_()
     c.error = err.data_ptr()
     _lib.check(lib.ts_run_conv_group(ctypes.byref(c), stream), "ts_run_conv_group")
-    e = int(err.item())
-    if e > 0:
-        raise OutOfBounds(g.src, e - 1)
-    if e < 0:
-        raise OutOfBounds(g.kern, -e - 1)
+    code, index, it = (int(v) for v in err.tolist())
+    if code:  # backstop: _compile checks every index on the host first
+        raise _annotate(OutOfBounds(g.src if code == 1 else g.kern, index),
+                        g.paths[it] if 0 <= it < len(g.paths) else "body")
     if g.tmp is not None and g.tmp in bufs:  # materialise the last iteration's temporary
         o = torch.from_numpy(g.b_off.astype(np.int64)).to(dev)
         vals = kern[:, (g.k_base[-1] + o).clamp(min=0)]
@@ -460,4 +578,4 @@ def run_program(p, inputs, extra_shapes=(), strict=False, lint_sink=None):
 
 
 __all__ = ["run_program", "run_program_batch", "UnsupportedProgram", "Buffer", "BufferStore",
-           "HARDWARE_SHAPES", "math"]
+           "HARDWARE_SHAPES"]

@@ -17,7 +17,6 @@ These definitions are restated independently in ``oracle/pipelines_ref.py``.
 
 from __future__ import annotations
 
-import math
 
 import numpy as np
 
@@ -96,4 +95,4 @@ def ceil_div(a: int, b: int) -> int:
 
 
 __all__ = ["lanczos3", "lanczos3_axis", "gaussian_taps", "box_taps", "conv_axis",
-           "downsample_offset", "ceil_div", "math"]
+           "downsample_offset", "ceil_div"]
