@@ -161,20 +161,6 @@ TS_API ts_status ts_axis_pass_ep(const ts_axis* a, int dim, int planes, int heig
 TS_API ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes,
                                    int out_dtype, int* out8);
 
-/* Which kernel ts_separable_run launches for these axes: 5 = strip kernel
- * (Toeplitz-like axes: uniform 16-output block spacing of 8/16/32 inputs;
- * the banded weights become one shifted strip per axis), 4 = block-tile
- * kernel (any banded axes).  The strip kernel is opt-in: only with the
- * environment variable TSB_STRIP=1 (it is slower than 4 on B200 today). */
-TS_API int ts_separable_variant(const ts_axis* rows, const ts_axis* cols, int planes, int out_dtype);
-
-/* Diagnostics: geometry of the last strip-kernel launch or variant query:
- * out16 = {valid, ring slots, K-steps rows, K-steps cols, output columns per
- * tile, staged columns, pass-1 N, edge slices rows, edge slices cols, work
- * units, row tiles per unit, smem bytes, V separate, D_H double, chunk
- * bytes, row tiles}.  Returns out16[0]. */
-TS_API int ts_strip_info(int* out16);
-
 /* Fused DCT-16 transform-domain denoise: 16x16 tiles at
  * stride 8, sine window folded into the DCT-II matrices, coring of every
  * non-DC coefficient (soft = 0: |c| < threshold -> 0; soft = 1: shrink by
@@ -193,11 +179,6 @@ TS_API ts_status ts_denoise_dct16_ep(const void* in, int64_t in_row_stride,
                                      int out_dtype, int planes, int height, int width,
                                      float threshold, int soft, const ts_epilogue* ep,
                                      void* stream);
-
-/* Diagnostics: subsequent ts_denoise_dct16 launches copy the TMEM
- * accumulators of CTA 0's first band (D1, D2, D3 per phase; D4) into
- * device_buffer (f32[4][2][128][256]); NULL turns it off. */
-TS_API ts_status ts_debug_dct16(float* device_buffer);
 
 /* One lowered convolution statement group of a tensorsel program, batched
  * over `instances` program instances (e.g. a difftest's seeds):
@@ -274,56 +255,6 @@ TS_API ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* s
  * f32, p*l entries) into out (device f32).  Replaces the Python double loop. */
 TS_API ts_status ts_matrix_for(int l, int k, int s, int p, const float* kernel, float* out, void* stream);
 
-/* Diagnostics: make subsequent ts_separable_run launches record clock64()
- * stamps for the first `tiles` tiles of CTAs [0, ctas) into device_buffer
- * (u64[ctas][tiles][10]; events: 0 producer ready, 1 stage free, 2 input
- * landed, 3 pass-1 issued, 4 D_V ready, 5 V operand written, 6 pass-2 start,
- * 7 pass-2 issued, 8 D_H ready, 9 output stored).  NULL turns it off. */
-TS_API ts_status ts_debug_trace(void* device_buffer, int ctas, int tiles);
-
-/* Diagnostics: one tcgen05 MMA  D(128 x n) = A(128 x k) · B(k x n)  with A
- * staged MN-major 128B-swizzled and B K-major interleaved exactly as the
- * separable kernel stages them.  a: row-major f32 (128 x k), b: row-major
- * f32 (k x n), d: row-major f32 (128 x n); all device pointers; k % 16 == 0,
- * n % 16 == 0, n <= 256, k <= 256. */
-TS_API ts_status ts_probe_umma(const float* a, const float* b, float* d, int k, int n, void* stream);
-
-/* Diagnostics: tcgen05 operand-mode probe.  D(128 x n) = A(128 x k) · B(k x n),
- * the K loop issued `reps` times into one accumulator; *cycles (device
- * pointer, may be NULL) receives clock64 cycles from first issue to
- * completion.  amode 0: A smem MN-major SW128 bf16, 1: A smem K-major bf16,
- * 2: A in TMEM f32 (kind::tf32); bmode 0: B smem K-major (bf16, f32 for
- * amode 2), 1: B smem MN-major SW128 bf16.  nacc > 1 round-robins the
- * repetitions over nacc accumulators (columns [n*i, n*i + n)) to measure
- * independent-MMA throughput; d then holds accumulator 0. */
-TS_API ts_status ts_probe_mma(int amode, int bmode, const float* a, const float* b, float* d,
-                              int k, int n, int reps, long long* cycles, int nacc, void* stream);
-
-/* Diagnostics: tcgen05.mma issue-rate microbenchmark (64 warp-converged,
- * elect-issued M=128 K=16 MMAs; variant 0..5 = N/accumulators (16,1) (16,8)
- * (64,1) (64,4) (256,1) (256,2)); *cycles (device) = cycles to completion. */
-TS_API ts_status ts_probe_issue(int variant, long long* cycles, void* stream);
-/* Same with A read from TMEM (TS mode); variant 0..3 = (N, kind) in
- * {(16, f16), (64, f16), (16, tf32), (64, tf32)}. */
-TS_API ts_status ts_probe_issue_ts(int variant, long long* cycles, void* stream);
-/* Streaming-operand issue rate: `count` elected M=128, K=16 MMAs cycling over
- * 8 K-slices; amode 0 smem MN-major SW128 / 1 smem K-major / 2 TMEM,
- * bmode 0 smem K-major / 1 smem MN-major SW128; nacc accumulators. */
-/* TMA streaming probe: grid CTAs stream a planes x H x W bf16 tensor in
- * chunks of rows x (64 * nbox) through an nr-slot ring (load path only). */
-TS_API ts_status ts_probe_tma(const void* src, int planes, int H, int W, int rows, int nbox, int nr,
-                              int grid, void* stream);
-/* TMEM load throughput probe: `warps` warps (multiple of 4) read `cols`
- * columns of their lane quarter `reps` times with tcgen05.ld.32x32b.x{x}. */
-TS_API ts_status ts_probe_tmem_ld(int x, int warps, int cols, int reps, long long* cycles,
-                                  void* stream);
-/* M = 64 accumulator layout probe: D (128 lanes x n, pre-filled with -1) after
- * one kind::f16 M=64 MMA (A 64 x 16, B 16 x n, row-major f32 in) issued at
- * TMEM lane lane_base; d receives all 128 lanes. */
-TS_API ts_status ts_probe_m64(const float* a, const float* b, float* d, int n, int lane_base,
-                              void* stream);
-TS_API ts_status ts_probe_issue2(int amode, int bmode, int n, int count, int nacc,
-                                 long long* cycles, void* stream);
 
 #ifdef __cplusplus
 }

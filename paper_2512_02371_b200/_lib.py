@@ -23,6 +23,7 @@ TS_AXIS_DC_EXACT = 0x1
 
 _lock = threading.Lock()
 _lib = None
+_diag = None
 
 
 class ConvGroup(ctypes.Structure):
@@ -78,33 +79,37 @@ _SIGNATURES = {
     "ts_separable_run_ep": (_I, [_P, _P, _I, _P, _I64, _I64, _I, _P, _I64, _I64, _I,
                                  ctypes.POINTER(Epilogue), _P]),
     "ts_separable_plan": (_I, [_P, _P, _I, _I, ctypes.POINTER(ctypes.c_int)]),
-    "ts_separable_variant": (_I, [_P, _P, _I, _I]),
     "ts_axis_pass": (_I, [_P, _I, _I, _I, _I, _P, _I64, _I64, _P, _I64, _I64, _I, _P]),
     "ts_axis_pass_ep": (_I, [_P, _I, _I, _I, _I, _P, _I64, _I64, _P, _I64, _I64, _I,
                              ctypes.POINTER(Epilogue), _P]),
-    "ts_strip_info": (_I, [ctypes.POINTER(ctypes.c_int)]),
-    "ts_probe_tma": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P]),
-    "ts_probe_tmem_ld": (_I, [_I, _I, _I, _I, _P, _P]),
-    "ts_probe_m64": (_I, [_P, _P, _P, _I, _I, _P]),
-    "ts_probe_issue2": (_I, [_I, _I, _I, _I, _I, _P, _P]),
     "ts_cast_f32_bf16": (_I, [_P, _P, _I64, _P]),
     "ts_separable_f32_ep": (_I, [_I, _P, _I, _I, _I64, _I64, _I, _I, _I, _P, _I, _I, _P, _I, _P,
                                  _I64, _I64, _I, _I, _P, _P]),
     "ts_run_conv_group": (_I, [_P, _P]),
-    "ts_debug_dct16": (_I, [_P]),
     "ts_denoise_dct16": (_I, [_P, _I64, _I64, _I, _P, _I64, _I64, _I, _I, _I, _I,
                               ctypes.c_float, _I, _P]),
     "ts_denoise_dct16_ep": (_I, [_P, _I64, _I64, _I, _P, _I64, _I64, _I, _I, _I, _I,
                                  ctypes.c_float, _I, ctypes.POINTER(Epilogue), _P]),
     "ts_matrix_for": (_I, [_I, _I, _I, _I, _P, _P, _P]),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+# Diagnostics (tools only): libtsb200_diag.so = the product sources built with
+# -DTSB_DIAG plus tools/diag/probe.cu; declared in tools/diag/tsb_diag.h.
+DIAG_LIB_PATH = os.path.join(_HERE, "_native", "libtsb200_diag.so")
+_DIAG_SIGNATURES = {
+    "ts_probe_tma": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P]),
+    "ts_probe_tmem_ld": (_I, [_I, _I, _I, _I, _P, _P]),
+    "ts_probe_m64": (_I, [_P, _P, _P, _I, _I, _P]),
+    "ts_probe_issue2": (_I, [_I, _I, _I, _I, _I, _P, _P]),
+    "ts_debug_dct16": (_I, [_P]),
     "ts_probe_umma": (_I, [_P, _P, _P, _I, _I, _P]),
     "ts_debug_trace": (_I, [_P, _I, _I]),
     "ts_probe_mma": (_I, [_I, _I, _P, _P, _P, _I, _I, _I, _P, _I, _P]),
     "ts_probe_issue": (_I, [_I, _P, _P]),
     "ts_probe_issue_ts": (_I, [_I, _P, _P]),
 }
-
-EXPORTED = tuple(_SIGNATURES)
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -131,6 +136,35 @@ def load(path: str | None = None):
         if path is None:
             _lib = lib
         return lib
+
+
+def load_diag():
+    """The diagnostics library (``make -C paper_2512_02371_b200/csrc diag``):
+    every product entry point plus trace hooks and micro-probes.  Tools
+    only; the product never loads it."""
+    global _diag
+    if os.path.abspath(LIB_PATH) == os.path.abspath(DIAG_LIB_PATH):
+        load()  # TSB_LIB_PATH points the product binding at the diag build (trace tools)
+    with _lock:
+        if _diag is None and _lib is not None and \
+                os.path.abspath(LIB_PATH) == os.path.abspath(DIAG_LIB_PATH):
+            for name, (res, args) in _DIAG_SIGNATURES.items():
+                fn = getattr(_lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _diag = _lib
+        if _diag is None:
+            if not os.path.exists(DIAG_LIB_PATH):
+                raise NativeLibraryMissing(
+                    f"diagnostics library not built: {DIAG_LIB_PATH} "
+                    "(run `make -C paper_2512_02371_b200/csrc diag`)")
+            lib = ctypes.CDLL(DIAG_LIB_PATH)
+            for name, (res, args) in {**_SIGNATURES, **_DIAG_SIGNATURES}.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _diag = lib
+        return _diag
 
 
 def last_error() -> str:

@@ -264,8 +264,8 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   if (in_rs < W || (in_rs * 2) % 16 || in_ps < in_rs * H || (in_ps * 2) % 16 || out_rs < OW ||
       (out_rs * oes) % 16 || out_ps < out_rs * OH || (out_ps * oes) % 16)
     return set_error(TS_ERR_INVALID, "axis_pass: strides");
-  cudaError_t de = cudaSetDevice(a->device);
-  if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
+  DeviceGuard guard(a->device);
+  if (guard.err != cudaSuccess) return cuda_error(guard.err, "cudaSetDevice");
   apass::Params P;
   P.ep = make_epik(ep);
   P.ax = a->dev();

@@ -281,12 +281,6 @@ void ts_axis_destroy(ts_axis* a) {
   if (a->d_ws) cudaFree(a->d_ws);
   if (a->d_tid) cudaFree(a->d_tid);
   if (a->d_tab) cudaFree(a->d_tab);
-  for (auto* sp : a->strip) {
-    if (!sp) continue;
-    if (sp->d_strip) cudaFree(sp->d_strip);
-    if (sp->d_specials) cudaFree(sp->d_specials);
-    delete sp;
-  }
   for (auto* m : a->merged) {
     if (!m) continue;
     if (m->d_tab) cudaFree(m->d_tab);

@@ -1,7 +1,6 @@
 // capi.cu — extern "C" entry points (include/tensorsel_b200.h) plus the small
-// device kernels that sit beside the fused executors: f32->bf16 cast, the
-// device-side dense Toeplitz builder (layout.matrix_for) and a tcgen05
-// descriptor probe used by the parity tests to pin the smem layouts.
+// device kernels that sit beside the fused executors: the f32->bf16 cast and
+// the device-side dense Toeplitz builder (layout.matrix_for).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -15,9 +14,9 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
                         int64_t out_ps, int out_dtype, const ts_epilogue* ep, cudaStream_t stream);
 ts_status separable_plan(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype,
                          int* out8);
+#ifdef TSB_DIAG
 void set_trace(void* buf, int ctas, int tiles);
-int separable_variant(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype);
-int strip_info(int* out16);
+#endif
 ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, const void* in,
                         int64_t in_rs, int64_t in_ps, void* out, int64_t out_rs, int64_t out_ps,
                         int out_dtype, const ts_epilogue* ep, cudaStream_t stream);
@@ -61,73 +60,6 @@ __global__ void matrix_for_kernel(int l, int k, int s, int p, int rows,
       if (t >= 0 && t < l) tap = t;
     }
     out[e] = tap >= 0 ? kern[tap] : 0.0f;
-  }
-}
-
-// ------------------------------------------------------------ UMMA probe
-__global__ void __launch_bounds__(128, 1)
-    probe_umma_kernel(const float* __restrict__ a, const float* __restrict__ b,
-                      float* __restrict__ d, int k, int n) {
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw_s = smem_u32(smem_raw);
-  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
-  uint8_t* base = smem_raw + (base_s - raw_s);
-  const uint32_t a_bytes = 128u * k * 2u;                   // two 64-wide m-atoms
-  const uint32_t b_bytes = static_cast<uint32_t>(k) * n * 2u;
-  uint8_t* sa = base;
-  uint8_t* sb = base + a_bytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + a_bytes + ((b_bytes + 1023u) & ~1023u));
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
-  const uint32_t lbo_a = static_cast<uint32_t>(k / 8) * 1024u;
-
-  // A (128 x k): MN-major, 128B swizzle — exactly the pass-1 staging layout
-  for (int e = threadIdx.x; e < 128 * k; e += blockDim.x) {
-    const int m = e / k, kk = e % k;
-    const uint32_t off = (m / 64) * lbo_a + (kk / 8) * 1024u + (kk % 8) * 128u +
-                         ((((m % 64) / 8) ^ (kk % 8)) * 16u) + (m % 8) * 2u;
-    *reinterpret_cast<__nv_bfloat16*>(sa + off) = __float2bfloat16_rn(a[e]);
-  }
-  // B (k x n): K-major, no swizzle, 8x8 core matrices
-  for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
-    const int kk = e / n, nn = e % n;
-    const uint32_t off = (nn / 8) * (k * 16u) + (kk / 8) * 128u + (nn % 8) * 16u + (kk % 8) * 2u;
-    *reinterpret_cast<__nv_bfloat16*>(sb + off) = __float2bfloat16_rn(b[e]);
-  }
-  fence_proxy_async_smem();
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    fence_barrier_init();
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0) tmem_alloc<256>(slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *slot;
-  if (threadIdx.x == 0) {
-    const uint32_t idesc = make_idesc(kFmtBF16, 128, n, 1, 0);
-    for (int q = 0; q < k / 16; ++q) {
-      const uint64_t ad = make_sdesc(base_s + q * 2048u, lbo_a, 1024u, kSwizzle128B);
-      const uint64_t bd = make_sdesc(base_s + a_bytes + q * 256u, 128u, k * 16u, kSwizzleNone);
-      mma_f16_ss(tmem, ad, bd, idesc, q > 0 ? 1u : 0u);
-    }
-    mma_commit(bar);
-  }
-  __syncwarp();
-  mbar_wait(bar, 0);
-  tc_fence_after();
-  const int row = warp * 32 + lane;
-  for (int c0 = 0; c0 < n; c0 += 16) {
-    uint32_t r[16];
-    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, r);
-    tmem_wait_ld();
-    for (int i = 0; i < 16; ++i) d[row * n + c0 + i] = __uint_as_float(r[i]);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc<256>(tmem);
   }
 }
 
@@ -175,10 +107,6 @@ ts_status ts_separable_plan(const ts_axis* rows, const ts_axis* cols, int planes
   return separable_plan(rows, cols, planes, out_dtype, out8);
 }
 
-int ts_separable_variant(const ts_axis* rows, const ts_axis* cols, int planes, int out_dtype) {
-  return separable_variant(rows, cols, planes, out_dtype);
-}
-
 ts_status ts_axis_pass(const ts_axis* a, int dim, int planes, int height, int width, const void* in,
                        int64_t in_row_stride, int64_t in_plane_stride, void* out,
                        int64_t out_row_stride, int64_t out_plane_stride, int out_dtype,
@@ -197,18 +125,20 @@ ts_status ts_axis_pass_ep(const ts_axis* a, int dim, int planes, int height, int
                        static_cast<cudaStream_t>(stream));
 }
 
-int ts_strip_info(int* out16) { return out16 ? strip_info(out16) : 0; }
-
+#ifdef TSB_DIAG
 ts_status ts_debug_trace(void* device_buffer, int ctas, int tiles) {
   if (device_buffer && (ctas < 1 || tiles < 1))
     return set_error(TS_ERR_INVALID, "trace: ctas and tiles must be >= 1");
   set_trace(device_buffer, ctas, tiles);
   return TS_OK;
 }
+#endif  // TSB_DIAG
 
 ts_status ts_cast_f32_bf16(const float* in, void* out, int64_t n, void* stream) {
   if (n < 0 || (n > 0 && (!in || !out))) return set_error(TS_ERR_INVALID, "cast: bad arguments");
   if (n == 0) return TS_OK;
+  DeviceGuard guard(device_of(in));
+  if (guard.err != cudaSuccess) return cuda_error(guard.err, "cudaSetDevice");
   int64_t blocks = (n / 8 + 255) / 256 + 1;
   if (blocks > 148 * 16) blocks = 148 * 16;
   cast_f32_bf16_kernel<<<static_cast<int>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
@@ -223,6 +153,8 @@ ts_status ts_matrix_for(int l, int k, int s, int p, const float* kernel, float* 
     return set_error(TS_ERR_INVALID, "ToeplitzSpec needs l, k, s, p >= 1");
   if (s != 1 && p != 1) return set_error(TS_ERR_INVALID, "stride and phases are exclusive");
   if (!kernel || !out) return set_error(TS_ERR_INVALID, "matrix_for: null pointer");
+  DeviceGuard guard(device_of(out));
+  if (guard.err != cudaSuccess) return cuda_error(guard.err, "cudaSetDevice");
   const int rows = p > 1 ? k / p + l : s * k + l;  // layout.matrix_rows (layout.py:54-57)
   const int64_t n = static_cast<int64_t>(rows) * k;
   int blocks = static_cast<int>((n + 255) / 256);
@@ -231,20 +163,6 @@ ts_status ts_matrix_for(int l, int k, int s, int p, const float* kernel, float* 
                                                                           out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "matrix_for kernel launch");
-}
-
-ts_status ts_probe_umma(const float* a, const float* b, float* d, int k, int n, void* stream) {
-  if (!a || !b || !d || k < 16 || k > 256 || k % 16 || n < 16 || n > 256 || n % 16)
-    return set_error(TS_ERR_INVALID, "probe: need k, n multiples of 16 in [16, 256]");
-  const uint32_t a_bytes = 128u * k * 2u;
-  const uint32_t b_bytes = static_cast<uint32_t>(k) * n * 2u;
-  const uint32_t smem = 1024 + a_bytes + ((b_bytes + 1023u) & ~1023u) + 64;
-  cudaError_t e = cudaFuncSetAttribute(probe_umma_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return cuda_error(e, "probe smem attribute");
-  probe_umma_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(a, b, d, k, n);
-  e = cudaGetLastError();
-  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe launch");
 }
 
 }  // extern "C"

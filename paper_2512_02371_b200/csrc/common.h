@@ -6,6 +6,8 @@
 #include <atomic>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "../../include/tensorsel_b200.h"
 
 namespace tsb {
@@ -51,28 +53,6 @@ struct MergedAxis {
   uint8_t* d_tiles = nullptr;
 };
 
-// Shift-invariant "strip" form of an axis for the v5 separable kernel
-// (csrc/strip.cpp): per tile, K-step q's operand slice equals a fixed strip
-// shifted by `shift` outputs per 16 inputs, except a few edge slices.
-struct StripPlan {
-  bool ok = false;
-  const char* why = "";
-  int role = 0;             // 0 rows (pass-1 A), 1 cols (pass-2 B)
-  int S = 0;                // input spacing between 16-output blocks
-  int shift = 0;            // outputs moved per 16-input K-step (multiple of 8)
-  int Q = 0;                // K-steps per tile
-  int G = 0;                // 8-output groups stored above output 0 in the strip
-  int nout = 0;             // outputs per tile (128 rows / NO cols)
-  int ntiles = 0;           // tiles along the axis
-  int staged = 0;           // cols role: input columns staged per tile (multiple of 64)
-  std::vector<int32_t> first_in;   // per tile: first input index of its window
-  std::vector<uint16_t> strip;     // (nout + 8G) x 16 bf16, K-major core matrices
-  std::vector<uint16_t> specials;  // nspec x (nout x 16) bf16, same layout
-  std::vector<int8_t> map;         // ntiles x Q: -1 strip, else special index
-  int nspec = 0;
-  uint8_t* d_strip = nullptr;
-  uint8_t* d_specials = nullptr;
-};
 }  // namespace tsb
 
 namespace tsb {
@@ -99,7 +79,6 @@ struct ts_axis {
   uint8_t* d_tiles = nullptr;
   std::vector<int32_t> tab;         // packed (ws << 16) | tid, nb + kBlockPad entries
   bool tab_ok = true;               // packing fits (|ws| < 32K, < 64K tiles)
-  mutable tsb::StripPlan* strip[2] = {nullptr, nullptr};  // lazily built per role
   mutable tsb::MergedAxis* merged[tsb::kMaxMerge + 1] = {};  // lazily built per factor
 
   tsb::AxisDev dev() const {
@@ -110,6 +89,32 @@ struct ts_axis {
 namespace tsb {
 ts_status set_error(ts_status st, const char* fmt, ...);
 ts_status cuda_error(int err, const char* what);
+
+// Scoped current-device switch: an entry point runs on the device its
+// operands live on and leaves the caller's current device as it found it.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Device that owns a device pointer (-1 if the runtime does not know it).
+inline int device_of(const void* p) {
+  cudaPointerAttributes a;
+  if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged ? a.device : -1;
+}
 // Byte offset of element (k, n) inside a K x 16 B tile (K-major, no swizzle:
 // 8x8 core matrices of 128 contiguous bytes; LBO = 128 B between k-chunks,
 // SBO = K*16 B between the two 8-column groups).

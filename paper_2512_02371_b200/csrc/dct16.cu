@@ -122,13 +122,16 @@ struct Params {
 // 4 D3 seen, 5 E3 done};
 // 7 MMA: band ready, 8 MMA: S1 issued (p=0); 22 E4 start, 23 E4 stored
 __device__ __forceinline__ void stamp(const Params& P, int it, int ev) {
+#ifdef TSB_DIAG
   if (P.trace != nullptr && static_cast<int>(blockIdx.x) < P.trace_ctas && it < P.trace_tiles)
     P.trace[(static_cast<size_t>(blockIdx.x) * P.trace_tiles + it) * 24 + ev] = clock64();
+#endif
 }
 
 // Diagnostics: copy `ncols` TMEM columns of this thread's lane to dbg.
 __device__ __forceinline__ void dbg_dump(const Params& P, int it, int stage, int p, uint32_t taddr,
                                          int row, int ncols) {
+#ifdef TSB_DIAG
   if (P.dbg == nullptr || blockIdx.x != 0 || it != 0) return;
   float* dst = P.dbg + ((static_cast<size_t>(stage) * 2 + p) * 128 + row) * 256;
   for (int c0 = 0; c0 < ncols; c0 += 16) {
@@ -137,6 +140,7 @@ __device__ __forceinline__ void dbg_dump(const Params& P, int it, int stage, int
     tmem_wait_ld();
     for (int i = 0; i < 16; ++i) dst[c0 + i] = __uint_as_float(r[i]);
   }
+#endif
 }
 
 __device__ __forceinline__ void mma_f16_ts_elect(uint32_t d, uint32_t a_tmem, uint64_t b,
@@ -776,6 +780,8 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
   if (in_rs < W || (in_rs * 2) % 16 || in_ps < in_rs * H || (in_ps * 2) % 16 || out_rs < W ||
       (out_rs * oes) % 16 || out_ps < out_rs * H || (out_ps * oes) % 16)
     return set_error(TS_ERR_INVALID, "dct16: strides");
+  DeviceGuard guard(device_of(in));
+  if (guard.err != cudaSuccess) return cuda_error(guard.err, "cudaSetDevice");
   static uint8_t* d_consts[64] = {nullptr};
   static std::mutex consts_mu;
   int dev = 0;
@@ -810,10 +816,12 @@ ts_status dct16_run(const void* in, int64_t in_rs, int64_t in_ps, int in_dtype, 
 
 }  // namespace tsb
 
-extern "C" ts_status ts_debug_dct16(float* device_buffer) {
+#ifdef TSB_DIAG
+extern "C" TS_API ts_status ts_debug_dct16(float* device_buffer) {
   tsb::dct_set_debug(device_buffer);
   return TS_OK;
 }
+#endif  // TSB_DIAG
 
 extern "C" ts_status ts_denoise_dct16(const void* in, int64_t in_row_stride, int64_t in_plane_stride,
                                       int in_dtype, void* out, int64_t out_row_stride,

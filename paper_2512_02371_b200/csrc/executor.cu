@@ -93,6 +93,8 @@ extern "C" ts_status ts_run_conv_group(const ts_conv_group* g, void* stream) {
     return set_error(TS_ERR_INVALID, "conv group: bad shape");
   const int64_t total = static_cast<int64_t>(g->instances) * g->m * g->n;
   if (total == 0) return TS_OK;
+  DeviceGuard guard(device_of(g->acc));
+  if (guard.err != cudaSuccess) return cuda_error(guard.err, "cudaSetDevice");
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   conv_group_kernel<<<static_cast<int>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(*g);

@@ -47,9 +47,6 @@ namespace tsb {
 
 const MergedAxis* axis_merged(const ts_axis* a, int m);
 int choose_merge(const ts_axis* a, int blocks);
-ts_status strip_run(const ts_axis* ra, const ts_axis* ca, int planes, const void* in, int64_t in_rs,
-                    int64_t in_ps, void* out, int64_t out_rs, int64_t out_ps, int out_dtype,
-                    cudaStream_t stream, bool dry);
 
 constexpr int kMaxStages = 4;
 constexpr int kThreads = 352;
@@ -96,9 +93,11 @@ __device__ __forceinline__ int tab_ws(int32_t e) { return e >> 16; }
 
 // Diagnostics: stamp event `ev` of tile `it` (events 0..9, see ts_debug_trace).
 __device__ __forceinline__ void trace_stamp(const SepParams& P, int it, int ev) {
+#ifdef TSB_DIAG
   if (P.trace != nullptr && static_cast<int>(blockIdx.x) < P.trace_ctas && it < P.trace_tiles &&
       (threadIdx.x & 31) == 0)
     P.trace[(static_cast<size_t>(blockIdx.x) * P.trace_tiles + it) * 10 + ev] = clock64();
+#endif
 }
 __device__ __forceinline__ int tab_tid(int32_t e) { return e & 0xFFFF; }
 
@@ -612,11 +611,13 @@ void get_trace(unsigned long long** buf, int* ctas, int* tiles) {
   *tiles = g_trace_tiles;
 }
 
+#ifdef TSB_DIAG
 void set_trace(void* buf, int ctas, int tiles) {
   g_trace = static_cast<unsigned long long*>(buf);
   g_trace_ctas = buf ? ctas : 0;
   g_trace_tiles = buf ? tiles : 0;
 }
+#endif  // TSB_DIAG
 
 static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, int oes,
                              SepParams& P) {
@@ -705,16 +706,8 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   if (ra->device != ca->device)
     return set_error(TS_ERR_INVALID, "separable: axes live on devices %d and %d", ra->device,
                      ca->device);
-  cudaError_t de = cudaSetDevice(ra->device);
-  if (de != cudaSuccess) return cuda_error(de, "cudaSetDevice");
-
-  // Toeplitz-like axes take the strip kernel (separable_strip.cu; opt-in,
-  // no epilogue variant)
-  if (!ep) {
-    ts_status s5 = strip_run(ra, ca, planes, in, in_rs, in_ps, out, out_rs, out_ps, out_dtype,
-                             stream, false);
-    if (s5 != TS_ERR_UNSUPPORTED) return s5;
-  }
+  DeviceGuard guard(ra->device);
+  if (guard.err != cudaSuccess) return cuda_error(guard.err, "cudaSetDevice");
 
   // launch parameters (block tables, smem plan) are cached per (axes, planes,
   // output size): rebuilding them costs more host time than a 1-frame launch
@@ -758,15 +751,6 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   if (st != TS_OK) return st;
   if (out_dtype == TS_BF16) return launch_sep<__nv_bfloat16>(P, tin, tout, stream, ep != nullptr);
   return launch_sep<float>(P, tin, tout, stream, ep != nullptr);
-}
-
-// Which kernel ts_separable_run would launch: 5 (strip) or 4 (block tiles).
-int separable_variant(const ts_axis* ra, const ts_axis* ca, int planes, int out_dtype) {
-  if (!ra || !ca) return -TS_ERR_INVALID;
-  int64_t rs = (ca->n_in + 7) / 8 * 8, ors = (ca->n_out + 7) / 8 * 8;
-  ts_status s5 = strip_run(ra, ca, planes < 1 ? 1 : planes, nullptr, rs, rs * ra->n_in, nullptr,
-                           ors, ors * ra->n_out, out_dtype, nullptr, true);
-  return s5 == TS_OK ? 5 : 4;
 }
 
 // The launch geometry a run would use (ts_separable_plan).

@@ -222,9 +222,15 @@ ts_status launch_f32(int planes, const float* in, int H, int W, int64_t irs, int
                      int64_t ors, int64_t ops, const EpiK& ek, cudaStream_t st) {
   constexpr int smem = Geo<S, T, OFF>::smem;
   auto fn = separable_f32_kernel<S, T, OFF, BF16, EXACT>;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (attr != cudaSuccess) return cuda_error(attr, "separable_f32: smem attribute");
+  static std::atomic<bool> attr_done[64] = {};  // the attribute is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return set_error(TS_ERR_INVALID, "separable_f32: device index");
+  if (!attr_done[dev].load()) {
+    cudaError_t attr = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) return cuda_error(attr, "separable_f32: smem attribute");
+    attr_done[dev].store(true);
+  }
   const int vec_ok = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && irs % 4 == 0 && ips % 4 == 0;
   dim3 grid((OW + kTC - 1) / kTC, (OH + kTR - 1) / kTR, planes);
   fn<<<grid, kThreads, smem, st>>>(in, H, W, irs, ips, vec_ok, out, OH, OW, ors, ops, rb, cb, rw,
@@ -270,6 +276,8 @@ extern "C" ts_status ts_separable_f32_ep(int planes, const float* in, int in_h, 
       out_row_stride < out_w || out_plane_stride < out_row_stride * out_h)
     return set_error(TS_ERR_INVALID, "separable_f32: strides smaller than the image");
   if (ep && ep->lo > ep->hi) return set_error(TS_ERR_INVALID, "epilogue: lo > hi");
+  DeviceGuard guard(device_of(in));
+  if (guard.err != cudaSuccess) return cuda_error(guard.err, "cudaSetDevice");
   const EpiK ek = make_epik(ep);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool bf = out_dtype == TS_BF16, exact = flags & TS_F32_EXACT;

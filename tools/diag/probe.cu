@@ -14,8 +14,77 @@
 
 #include "common.h"
 #include "sm100.cuh"
+#include "tsb_diag.h"
 
 namespace tsb {
+
+// ------------------------------------------------------------ UMMA probe
+__global__ void __launch_bounds__(128, 1)
+    probe_umma_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                      float* __restrict__ d, int k, int n) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_s = smem_u32(smem_raw);
+  const uint32_t base_s = (raw_s + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_s - raw_s);
+  const uint32_t a_bytes = 128u * k * 2u;                   // two 64-wide m-atoms
+  const uint32_t b_bytes = static_cast<uint32_t>(k) * n * 2u;
+  uint8_t* sa = base;
+  uint8_t* sb = base + a_bytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + a_bytes + ((b_bytes + 1023u) & ~1023u));
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const uint32_t lbo_a = static_cast<uint32_t>(k / 8) * 1024u;
+
+  // A (128 x k): MN-major, 128B swizzle — exactly the pass-1 staging layout
+  for (int e = threadIdx.x; e < 128 * k; e += blockDim.x) {
+    const int m = e / k, kk = e % k;
+    const uint32_t off = (m / 64) * lbo_a + (kk / 8) * 1024u + (kk % 8) * 128u +
+                         ((((m % 64) / 8) ^ (kk % 8)) * 16u) + (m % 8) * 2u;
+    *reinterpret_cast<__nv_bfloat16*>(sa + off) = __float2bfloat16_rn(a[e]);
+  }
+  // B (k x n): K-major, no swizzle, 8x8 core matrices
+  for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
+    const int kk = e / n, nn = e % n;
+    const uint32_t off = (nn / 8) * (k * 16u) + (kk / 8) * 128u + (nn % 8) * 16u + (kk % 8) * 2u;
+    *reinterpret_cast<__nv_bfloat16*>(sb + off) = __float2bfloat16_rn(b[e]);
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) tmem_alloc<256>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc(kFmtBF16, 128, n, 1, 0);
+    for (int q = 0; q < k / 16; ++q) {
+      const uint64_t ad = make_sdesc(base_s + q * 2048u, lbo_a, 1024u, kSwizzle128B);
+      const uint64_t bd = make_sdesc(base_s + a_bytes + q * 256u, 128u, k * 16u, kSwizzleNone);
+      mma_f16_ss(tmem, ad, bd, idesc, q > 0 ? 1u : 0u);
+    }
+    mma_commit(bar);
+  }
+  __syncwarp();
+  mbar_wait(bar, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  for (int c0 = 0; c0 < n; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, r);
+    tmem_wait_ld();
+    for (int i = 0; i < 16; ++i) d[row * n + c0 + i] = __uint_as_float(r[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
 
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
                                             uint32_t idesc, uint32_t accumulate) {
@@ -723,3 +792,18 @@ extern "C" ts_status ts_probe_m64(const float* a, const float* b, float* d, int 
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "probe_m64 launch");
 }
+
+extern "C" TS_DIAG_API ts_status ts_probe_umma(const float* a, const float* b, float* d, int k, int n, void* stream) {
+  if (!a || !b || !d || k < 16 || k > 256 || k % 16 || n < 16 || n > 256 || n % 16)
+    return set_error(TS_ERR_INVALID, "probe: need k, n multiples of 16 in [16, 256]");
+  const uint32_t a_bytes = 128u * k * 2u;
+  const uint32_t b_bytes = static_cast<uint32_t>(k) * n * 2u;
+  const uint32_t smem = 1024 + a_bytes + ((b_bytes + 1023u) & ~1023u) + 64;
+  cudaError_t e = cudaFuncSetAttribute(probe_umma_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_error(e, "probe smem attribute");
+  probe_umma_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(a, b, d, k, n);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : cuda_error(e, "probe launch");
+}
+

@@ -3,7 +3,7 @@ import os as _os, sys as _sys
 _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import torch
 from paper_2512_02371_b200 import _lib
-L = _lib.load()
+L = _lib.load_diag()
 g = torch.Generator().manual_seed(0)
 n = 32
 a = torch.randn(64, 16, generator=g).bfloat16().float().cuda()

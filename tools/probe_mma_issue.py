@@ -2,7 +2,7 @@ import os as _os, sys as _sys
 _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import torch, json
 from paper_2512_02371_b200 import _lib
-L = _lib.load()
+L = _lib.load_diag()
 c = torch.zeros(1, dtype=torch.int64, device="cuda")
 cases = []
 for am, bm in ((0, 0), (1, 0), (0, 1), (1, 1), (2, 0), (2, 1)):

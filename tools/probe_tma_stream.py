@@ -2,7 +2,7 @@ import os as _os, sys as _sys
 _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import json, torch
 from paper_2512_02371_b200 import _lib
-L = _lib.load()
+L = _lib.load_diag()
 x = torch.rand((48, 2160, 3840), device="cuda").bfloat16()
 def run(rows, nbox, nr, grid=148, n=10):
     f = lambda: _lib.check(L.ts_probe_tma(x.data_ptr(), 48, 2160, 3840, rows, nbox, nr, grid, None))
