@@ -92,52 +92,66 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled in-process through
+    NVML every `period` seconds on a background thread while the GPU is
+    under load.  `mark()` splits the samples into the pre-roll (the loaded
+    warm-up just before the timed region) and the timed region itself, so
+    even a few-millisecond timed region reports clocks under load."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("sw_power_cap", 0x4), ("hw_power_brake", 0x80))
 
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.proc = None
-        self.path = None
+    def __init__(self, gpu_index, period=0.002):
+        self.gpu, self.period = gpu_index, period
+        self.samples, self.t_mark = [], None
+        self._stop = None
+        self._th = None
 
     def start(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.gpu)],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: report why instead of inventing clocks
+            self.err = f"nvml unavailable: {e}"
+            return
+        self.err = None
+        self._stop = threading.Event()
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    break
+                self.samples.append((time.perf_counter(), mhz, rs))
+                time.sleep(self.period)
+
+        self._th = threading.Thread(target=loop, daemon=True)
+        self._th.start()
+
+    def mark(self):
+        self.t_mark = time.perf_counter()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
-                    "samples": 0}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        rows = []
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
-        os.unlink(self.path)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+        if self._stop is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err], "samples": 0}
+        self._stop.set()
+        self._th.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        timed = [x for x in self.samples if self.t_mark is not None and x[0] >= self.t_mark]
+        mhz = [m for _, m, _ in self.samples]
+        reasons = sorted({n for _, _, r in self.samples for n, bit in self.REASONS if r & bit})
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples),
+                "samples_timed": len(timed),
+                "sm_mhz_timed": statistics.median([m for _, m, _ in timed]) if timed else None,
+                "source": f"NVML every {self.period * 1e3:.0f} ms over the loaded pre-roll "
+                          "(>= 0.5 s) and the timed region"}
 
 
 # --------------------------------------------------------------- B200 arm
@@ -205,18 +219,27 @@ def run_b200(args):
           for _ in range(K)]
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.05)
+    # loaded pre-roll (untimed) so the clock samples see the GPU under this
+    # load even when the timed region is a few milliseconds long
+    t_pre = time.perf_counter()
+    while time.perf_counter() - t_pre < 0.5:
+        for i in range(16):
+            y = fn(xs[i % 2])
+        torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    clocks.mark()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("bench.timed")
     t0.record(stream)
     for i in range(K):
         ev[i][0].record(stream)
         y = fn(xs[i % 2])
         ev[i][1].record(stream)
     t1.record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -255,10 +278,12 @@ def run_b200(args):
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("bench.e2e")
     e0.record(stream)
     for _ in range(E):
         e2e_step()
     e1.record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / E], device=dev, dtype=torch.float64)
     if ws > 1:
@@ -341,32 +366,70 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+_CPU = {}
+
+
+def _cpu_band(band):
+    """One output row band of the oracle pipeline (worker process; numpy
+    single-threaded): the band's input rows plus halo are sliced from the
+    full image, the row axis keeps the full image's clamp-to-edge."""
+    from oracle import pipelines_ref as R
+    img, op, taps, oh, ow = (_CPU[k] for k in ("img", "op", "taps", "oh", "ow"))
+    o0, o1 = band
+    H, W = img.shape[-2:]
+    if op == "dct16":  # 8-row halo: every kept output row sees both its tile rows
+        i0, i1 = max(o0 - 8, 0), min(o1 + 8, H)
+        return R.dct_denoise(img[:, i0:i1], 0.15, "hard")[:, o0 - i0:o0 - i0 + (o1 - o0)]
+    if op in ("lanczos", "lanczos+gauss"):  # (c5's 9-tap filter runs on the assembled frame)
+        rows, cols = R.lanczos3_weights(H, oh), R.lanczos3_weights(W, ow)
+    else:
+        k = R.gaussian_kernel(taps)
+        rows, cols = R.centred_axis(H, k), R.centred_axis(W, k)
+    f, w = rows
+    idx = np.clip(f[o0:o1, None] + np.arange(w.shape[1])[None, :], 0, H - 1)
+    i0, i1 = int(idx.min()), int(idx.max()) + 1
+    h = R.axis_pass(img[:, i0:i1], cols[0], cols[1], axis=-1)
+    return R.axis_pass(h, np.asarray(f[o0:o1]) - i0, w[o0:o1], axis=-2)
+
+
 def cpu_baseline(cfg):
-    """The oracle (numpy restatement, 1 thread) on a bounded sample."""
+    """The oracle (numpy restatement) on a bounded sample, spread over all
+    host cores: output row bands of the frame, one process per core."""
+    import multiprocessing as mp
     from oracle import pipelines_ref
     H, W, oh, ow, op, taps, _ = CONFIGS[cfg]
     rng = np.random.default_rng(SEED)
     planes = 3 if H * W <= 2160 * 3840 else 1
     img = rng.random((planes, H, W), dtype=np.float32)
+    cores = os.cpu_count() or 1
+    n_out = H if op in ("dct16", "gauss") else oh
+    step = 8 if op == "dct16" else 1
+    nb = max(1, min(cores * 4, n_out // max(step, 16)))
+    edges = [(i * n_out // nb) // step * step for i in range(nb)] + [n_out]
+    bands = [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+    _CPU.update(img=img, op=op, taps=taps, oh=oh, ow=ow)
+    env_threads = os.environ.get("OMP_NUM_THREADS")
+    os.environ["OMP_NUM_THREADS"] = "1"
+    ctx = mp.get_context("fork")
     t = time.perf_counter()
     reps = 0
-    while True:  # a bounded sample of ~10 s of CPU work (at least one pass)
-        if op == "lanczos":
-            pipelines_ref.resample(img, oh, ow)
-        elif op == "lanczos+gauss":
-            pipelines_ref.gaussian_blur(pipelines_ref.resample(img, oh, ow), taps)
-        elif op == "dct16":
-            pipelines_ref.dct_denoise(img, 0.15, "hard")
-        else:
-            pipelines_ref.gaussian_blur(img, taps)
-        reps += 1
-        dt = time.perf_counter() - t
-        if dt >= 10.0:
-            break
-    return {"value": round(reps * H * W * planes / 3 / dt / 1e6, 3), "unit": "Mpixel/s", "cores": 1,
-            "kind": "port",
-            "sample": f"oracle/pipelines_ref, {reps} pass(es) over {planes} plane(s) of {H}x{W} "
-                      f"({dt:.1f} s, 1 thread)"}
+    with ctx.Pool(cores) as pool:
+        while True:  # a bounded sample of ~10 s of CPU work (at least one pass)
+            parts = pool.map(_cpu_band, bands)
+            if op == "lanczos+gauss":  # the 9-tap filter over the assembled 1080p frame
+                pipelines_ref.gaussian_blur(np.concatenate(parts, axis=-2), taps)
+            reps += 1
+            dt = time.perf_counter() - t
+            if dt >= 10.0:
+                break
+    if env_threads is None:
+        os.environ.pop("OMP_NUM_THREADS", None)
+    else:
+        os.environ["OMP_NUM_THREADS"] = env_threads
+    return {"value": round(reps * H * W * planes / 3 / dt / 1e6, 3), "unit": "Mpixel/s",
+            "cores": cores, "kind": "port",
+            "sample": f"oracle/pipelines_ref over {len(bands)} output row bands of {planes} "
+                      f"plane(s) of {H}x{W}, {reps} pass(es) in {dt:.1f} s, {cores} processes"}
 
 
 # ---------------------------------------------------------- reference arm
@@ -500,11 +563,35 @@ def run_reference_port(args, cores):
                 "d2h_bytes_per_step": 0}}))
 
 
+def launch_ranks(args):
+    """`bench.py --gpus N` without a torchrun environment: relaunch this
+    script under torch.distributed.run with N ranks (one process per GPU) and
+    pass its output through.  Returns the exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and args.gpus > 1:
+        sys.exit(launch_ranks(args))
+    if ws and ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; refusing to time a "
+                 "different number of GPUs than asked for")
     if args.impl == "reference":
         run_reference(args)
     else:
+        import torch
+        if torch.cuda.device_count() < max(1, args.gpus):
+            sys.exit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} "
+                     "CUDA device(s) are visible")
         run_b200(args)
 
 

@@ -11,6 +11,14 @@ barriers / timing and for gathering results outside the timed region.
   so clamp-to-edge still refers to the true image edges.
 * :class:`FrameSharder` — runs a pipeline over a rank's frame shard in
   chunks, on the rank's own GPU and stream.
+* :func:`run_sharded`  — one process driving several GPUs: a batch of
+  frames in pinned host memory is split into contiguous frame shards, each
+  streamed host -> device -> host on its own device (own streams, own
+  weight-axis cache) with no inter-GPU traffic.
+* :func:`separable_bands` / :func:`resample_bands` — one large image split
+  into output row bands, one per device: each device reads its band plus a
+  read-only halo, runs the fused kernel on a band-local rows axis and writes
+  disjoint output rows.
 """
 
 from __future__ import annotations
@@ -27,11 +35,14 @@ def frame_shard(n_frames: int, world_size: int, rank: int):
     return start, base + (1 if rank < extra else 0)
 
 
-def row_bands(first, taps: int, n_in: int, world_size: int, rank: int, align: int = 16):
+def row_bands(first, taps: int, n_in: int, world_size: int, rank: int, align: int = 16,
+              in_align: int = 16):
     """Split the outputs of an axis into `world_size` bands (multiples of
     `align` rows except the last) and return rank's
     (out_start, out_stop, in_start, in_stop) — the input rows its outputs
-    read, clamped to the image."""
+    read, clamped to the image.  in_start is rounded down to a multiple of
+    `in_align`, so the band-local axis keeps the full axis's window
+    alignment (the builder places 16-output windows on multiples of 8)."""
     first = np.asarray(first)
     n_out = len(first)
     blocks = -(-n_out // align)
@@ -41,7 +52,8 @@ def row_bands(first, taps: int, n_in: int, world_size: int, rank: int, align: in
         return o0, o0, 0, 0
     lo = int(first[o0:o1].min())
     hi = int(first[o0:o1].max()) + taps
-    return o0, o1, max(lo, 0), min(hi, n_in)
+    lo = max(lo, 0) // in_align * in_align
+    return o0, o1, lo, min(hi, n_in)
 
 
 def band_axis(first, weights, n_in: int, out_start: int, out_stop: int, in_start: int,
@@ -134,3 +146,86 @@ class FrameSharder:
             return out
         import torch
         return torch.cat(results, 0) if results else None
+
+
+def run_sharded(fn, host_in, host_out, devices, *, planes_per_frame: int = 3,
+                chunk_planes: int = 12):
+    """Run `fn` (a pipeline of :mod:`pipelines`) over a batch of frames held in
+    (pinned) host memory on several devices from ONE process: frame shards
+    (:func:`frame_shard`) go to ``devices`` in order, each streamed through
+    :func:`pipelines.run_from_host` on that device (its own copy/compute
+    streams and weight-axis cache).  All shards are enqueued before any is
+    waited on, so the devices run concurrently; returns host_out once every
+    device has finished.  No data moves between devices."""
+    import torch
+
+    from . import pipelines
+    devices = [int(d) for d in devices]
+    if not devices:
+        raise ValueError("run_sharded needs at least one device")
+    P = host_in.shape[0]
+    if P % planes_per_frame:
+        raise ValueError(f"{P} planes is not a whole number of {planes_per_frame}-plane frames")
+    n_frames = P // planes_per_frame
+    done = []
+    for r, d in enumerate(devices):
+        s, c = frame_shard(n_frames, len(devices), r)
+        if c == 0:
+            continue
+        lo, hi = s * planes_per_frame, (s + c) * planes_per_frame
+        with torch.cuda.device(d):
+            pipelines.run_from_host(fn, host_in[lo:hi], host_out[lo:hi], chunk_planes=chunk_planes)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(d))
+            done.append(ev)
+    for ev in done:
+        ev.synchronize()
+    return host_out
+
+
+def separable_bands(x, rows, cols, n_out_rows: int, n_out_cols: int, devices, *,
+                    out_dtype=None):
+    """One large image (planes x H x W, on any device) as output row bands,
+    one per entry of ``devices``: band r reads input rows [in_start, in_stop)
+    (its outputs' taps, clamped to the image) and writes output rows
+    [out_start, out_stop).  rows / cols are (first, weights) of the two
+    axes over the FULL image; each band runs the fused kernel on a
+    band-local rows axis (:func:`band_axis`).  Returns the assembled output
+    on x's device."""
+    import torch
+
+    from . import axis as _axis, pipelines
+    H, W = x.shape[-2:]
+    rf, rw = np.asarray(rows[0]), np.asarray(rows[1], np.float32)
+    cf, cw = np.asarray(cols[0]), np.asarray(cols[1], np.float32)
+    taps = rw.shape[1]
+    out_dtype = out_dtype or x.dtype
+    out = torch.empty(x.shape[:-2] + (n_out_rows, n_out_cols), dtype=out_dtype, device=x.device)
+    parts = []
+    for r, d in enumerate(devices):
+        o0, o1, i0, i1 = row_bands(rf, taps, H, len(devices), r)
+        if o0 >= o1:
+            continue
+        bf, bw, bn = band_axis(rf, rw, H, o0, o1, i0, i1)
+        # cached: an Axis frees its device tiles when collected, and the
+        # band's kernel is still in flight when this function returns
+        ra = _axis.cached(("band", bn, o1 - o0, bf.tobytes(), bw.tobytes(), int(d)),
+                          lambda: _axis.Axis(bn, o1 - o0, bf, bw, device=int(d)))
+        ca = _axis.cached(("cols", W, n_out_cols, cf.tobytes(), cw.tobytes(), int(d)),
+                          lambda d=d: _axis.Axis(W, n_out_cols, cf, cw, device=int(d)))
+        with torch.cuda.device(int(d)):
+            xb = x[..., i0:i1, :].to(f"cuda:{int(d)}", non_blocking=True)
+            yb = pipelines.separable(xb, ra, ca, out_dtype=out_dtype)
+        parts.append((o0, o1, yb))
+    for o0, o1, yb in parts:
+        out[..., o0:o1, :].copy_(yb, non_blocking=True)
+    return out
+
+
+def resample_bands(x, out_h: int, out_w: int, devices, *, out_dtype=None):
+    """Lanczos-3 resample of one large image split into row bands over
+    ``devices`` (:func:`separable_bands`)."""
+    from . import filters
+    H, W = x.shape[-2:]
+    return separable_bands(x, filters.lanczos3_axis(H, out_h), filters.lanczos3_axis(W, out_w),
+                           out_h, out_w, devices, out_dtype=out_dtype)
