@@ -107,6 +107,78 @@ def layout_fixtures(rng):
     return out
 
 
+def mm_program(n_tiles, fixed_left):
+    """C_t = A_t · B_t for n_tiles 16x16 tiles as a For loop of
+    wmma_load_a / wmma_load_b / wmma_mma / wmma_store (the lowered-conv
+    intrinsics, interp.py:419-486).  fixed_left: A is one 16x16 matrix and B
+    varies per tile, else A varies and B is fixed."""
+    R = "(ramp (imm i32 0) (imm i32 1) 256)"
+    base = "(mul (var t) (imm i32 256))"
+    a_len, b_len = (256, 256 * n_tiles) if fixed_left else (256 * n_tiles, 256)
+    a_base, b_base = ("(imm i32 0)", base) if fixed_left else (base, "(imm i32 0)")
+    return ir.parse_program(f"""(param A f32 {a_len} mem)
+(param B f32 {b_len} mem)
+(param O f32 {256 * n_tiles} mem)
+(wmma-shape 16 16 16)
+(allocate acc f32 256 wmma)
+(for t 0 {n_tiles}
+ (store acc {R} (call wmma_zero (imm i32 16) (imm i32 16)))
+ (store acc {R} (call wmma_mma (call wmma_load_a (var A) {a_base} (imm i32 16) (imm i32 16) (imm i32 16)) (call wmma_load_b (var B) {b_base} (imm i32 16) (imm i32 16) (imm i32 16)) (load acc (f32 256) {R})))
+ (evaluate (call wmma_store (var O) {base} (imm i32 16) (imm i32 16) (load acc (f32 256) {R}))))
+""")
+
+
+def ref_mm(A, B, fixed_left):
+    """Run mm_program through interp.run_program (strict hardware shapes)."""
+    tiles = B if fixed_left else A
+    n = tiles.shape[0]
+    prog = mm_program(n, fixed_left)
+    st = interp.run_program(prog, {"A": np.ascontiguousarray(A, np.float32).reshape(-1),
+                                   "B": np.ascontiguousarray(B, np.float32).reshape(-1),
+                                   "O": np.zeros(256 * n, np.float32)}, strict=True)
+    return st["O"].data.reshape(n, 16, 16).copy()
+
+
+def dct_fixtures(arrays, kats, rng):
+    P, H, W = 2, 40, 56
+    yy, xx = np.mgrid[0:H, 0:W]
+    clean = 0.5 + 0.4 * np.sin(xx / 7.0) * np.cos(yy / 5.0)
+    img = interp.round_bf16(np.clip(clean + rng.normal(0, 0.05, (P, H, W)), 0, 1).astype(np.float32))
+    arrays["dct_img"] = img
+    n, h = 16, 8
+    k = np.arange(n)[:, None]
+    m = np.arange(n)[None, :]
+    D = np.cos(np.pi * (2 * m + 1) * k / (2 * n)) * np.sqrt(2.0 / n)
+    D[0, :] = np.sqrt(1.0 / n)
+    w = np.sin(np.pi * (np.arange(n) + 0.5) / n)
+    Dw = (D * w[None, :]).astype(np.float32)
+    arrays["dct_Dw"] = Dw
+    xp = np.pad(img, ((0, 0), (h, h), (h, h)), mode="edge")
+    ty, tx = H // h + 1, W // h + 1
+    T = np.stack([xp[p, h * i:h * i + n, h * j:h * j + n]
+                  for p in range(P) for i in range(ty) for j in range(tx)])
+    C = ref_mm(ref_mm(Dw, T, True), np.ascontiguousarray(Dw.T), False)
+    arrays["dct_coeffs"] = C.reshape(P, ty, tx, n, n)
+    thr = 0.15
+    for mode in ("hard", "soft", "zero"):
+        Cc = C.copy()
+        if mode == "hard":
+            Cc = np.where(np.abs(C) < np.float32(thr), np.float32(0), C).astype(np.float32)
+        elif mode == "soft":
+            Cc = (np.sign(C) * np.maximum(np.abs(C) - np.float32(thr), np.float32(0))).astype(np.float32)
+        Cc[:, 0, 0] = C[:, 0, 0]
+        Rt = ref_mm(ref_mm(np.ascontiguousarray(Dw.T), Cc, True), Dw, False).reshape(P, ty, tx, n, n)
+        out = np.zeros((P, H + 2 * h, W + 2 * h), np.float32)
+        for py in range(2):  # each pixel: ((0 + t00) + t01) + t10) + t11, phase order
+            for px in range(2):
+                for i in range(py, ty, 2):
+                    for j in range(px, tx, 2):
+                        out[:, h * i:h * i + n, h * j:h * j + n] += Rt[:, i, j]
+        arrays[f"dct_out_{mode}"] = out[:, h:h + H, h:h + W].copy()
+    kats["dct"] = {"threshold": thr, "tiles_per_plane": [ty, tx], "planes": P,
+                   "wmma_shape": [16, 16, 16], "strict": True}
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     rng = np.random.default_rng(0x251202371)
@@ -228,6 +300,11 @@ def main():
     arrays["colwalk_K"] = interp.round_bf16(w[10])
     arrays["colwalk_out"] = run(prog, arrays["colwalk_K"], img.reshape(-1))
     kats["colwalk"] = {"col": col, "W": W, "stride": 2, "n_out": 8}
+
+    # -- DCT-16 denoise: the four 16x16x16 products per tile run by the
+    #    reference as wmma_mma programs (strict: the hardware shape 16x16x16,
+    #    interp.py:25-29); tiles, coring and overlap-add are numpy glue here
+    dct_fixtures(arrays, kats, rng)
 
     # -- layout
     kats["layout"] = layout_fixtures(rng)

@@ -133,6 +133,88 @@ def sine_window(n=16):
     return np.sin(np.pi * (np.arange(n) + 0.5) / n)
 
 
+def dct_window_matrix(n=16):
+    """Dw = D·diag(w) in f32 (the analysis / synthesis matrix of a tile)."""
+    return (dct_matrix(n) * sine_window(n)[None, :]).astype(np.float32)
+
+
+def mm_left(A, B):
+    """A (n x n) times every tile B (..., n, n) with interp's wmma_mma
+    arithmetic (interp.py:459-486): f32 products, k summed left to right
+    from k = 0, then C + s with C = 0."""
+    A = np.asarray(A, np.float32)
+    B = np.asarray(B, np.float32)
+    s = (A[:, 0][:, None] * B[..., 0:1, :]).astype(np.float32)
+    for k in range(1, A.shape[1]):
+        s = (s + A[:, k][:, None] * B[..., k:k + 1, :]).astype(np.float32)
+    return (np.float32(0.0) + s).astype(np.float32)
+
+
+def mm_right(A, B):
+    """Every tile A (..., n, n) times B (n x n), wmma_mma arithmetic."""
+    A = np.asarray(A, np.float32)
+    B = np.asarray(B, np.float32)
+    s = (A[..., :, 0:1] * B[0, :]).astype(np.float32)
+    for k in range(1, B.shape[0]):
+        s = (s + A[..., :, k:k + 1] * B[k, :]).astype(np.float32)
+    return (np.float32(0.0) + s).astype(np.float32)
+
+
+def dct_tiles(img, n=16):
+    """(planes, ty, tx, n, n) f32 tiles at stride n/2 over the image extended
+    by n/2 on each side with clamp-to-edge; planes flattened."""
+    x = np.asarray(img, np.float32)
+    h = n // 2
+    H, W = x.shape[-2:]
+    if H % h or W % h:
+        raise ValueError(f"image {H}x{W} must be a multiple of {h}")
+    x = x.reshape((-1, H, W))
+    xp = np.pad(x, ((0, 0), (h, h), (h, h)), mode="edge")
+    ty, tx = H // h + 1, W // h + 1
+    s = xp.strides
+    return np.lib.stride_tricks.as_strided(
+        xp, shape=(x.shape[0], ty, tx, n, n), strides=(s[0], s[1] * h, s[2] * h, s[1], s[2])).copy()
+
+
+def dct_coefficients(img, n=16):
+    """Forward transform of every tile: C = (Dw · T) · Dwᵀ, two wmma_mma
+    products per tile (pinned bitwise to reference-run programs,
+    tests/golden dct_*)."""
+    Dw = dct_window_matrix(n)
+    return mm_right(mm_left(Dw, dct_tiles(img, n)), np.ascontiguousarray(Dw.T))
+
+
+def dct_core(C, threshold, mode):
+    """Coring of every non-DC coefficient (hard: |c| < threshold -> 0; soft:
+    shrink towards 0 by threshold); f32."""
+    C = np.asarray(C, np.float32)
+    dc = C[..., 0, 0].copy()
+    if mode == "hard":
+        C = np.where(np.abs(C) < threshold, np.float32(0), C).astype(np.float32)
+    elif mode == "soft":
+        C = (np.sign(C) * np.maximum(np.abs(C) - np.float32(threshold), np.float32(0))).astype(np.float32)
+    else:
+        raise ValueError(mode)
+    C[..., 0, 0] = dc
+    return C
+
+
+def dct_overlap_add(R, H, W, n=16):
+    """Overlap-add of the inverse tiles R (planes, ty, tx, n, n): each output
+    pixel is the f32 sum of its four tiles in phase order (0,0), (0,1),
+    (1,0), (1,1), starting from 0; returns (planes, H, W)."""
+    h = n // 2
+    P = R.shape[0]
+    out = np.zeros((P, H + 2 * h, W + 2 * h), np.float32)
+    for py in range(2):
+        for px in range(2):
+            sub = R[:, py::2, px::2]
+            ny, nx = sub.shape[1], sub.shape[2]
+            blk = sub.transpose(0, 1, 3, 2, 4).reshape(P, ny * n, nx * n)
+            out[:, py * h:py * h + ny * n, px * h:px * h + nx * n] += blk
+    return out[:, h:h + H, h:h + W]
+
+
 def dct_denoise(img, threshold, mode="hard", n=16):
     """Transform-domain coring, restated.
 
@@ -142,37 +224,37 @@ def dct_denoise(img, threshold, mode="hard", n=16):
     soft: shrink towards 0 by threshold; the DC bin is always kept), inverse
     transformed with the same window (Dwᵀ C Dw) and overlap-added.  With
     threshold 0 the output equals the input (up to f32 rounding).
-    Image height/width must be multiples of n/2."""
+    Image height/width must be multiples of n/2.
+
+    The four 16x16x16 products per tile are interp's wmma_mma (f32 products,
+    left-to-right k, + 0): pinned bitwise to programs run by the reference
+    (oracle/make_golden.py, tests/golden dct_*); tiling, coring and the
+    overlap-add order are this restatement's choices (the reference has no
+    code for them)."""
     x = np.asarray(img, np.float32)
-    h = n // 2
     H, W = x.shape[-2:]
-    if H % h or W % h:
-        raise ValueError(f"image {H}x{W} must be a multiple of {h}")
     lead = x.shape[:-2]
-    x = x.reshape((-1, H, W))
-    D = dct_matrix(n)
-    w = sine_window(n)
-    Dw = (D * w[None, :]).astype(np.float32)
-    xp = np.pad(x, ((0, 0), (h, h), (h, h)), mode="edge")
-    ty, tx = H // h + 1, W // h + 1
-    s = xp.strides
-    tiles = np.lib.stride_tricks.as_strided(
-        xp, shape=(x.shape[0], ty, tx, n, n), strides=(s[0], s[1] * h, s[2] * h, s[1], s[2]))
-    C = np.einsum("km,ptxmn,ln->ptxkl", Dw, tiles, Dw, optimize=True).astype(np.float32)
-    dc = C[..., 0, 0].copy()
-    if mode == "hard":
-        C = np.where(np.abs(C) < threshold, np.float32(0), C)
-    elif mode == "soft":
-        C = np.sign(C) * np.maximum(np.abs(C) - threshold, 0)
-    else:
-        raise ValueError(mode)
-    C[..., 0, 0] = dc
-    T = np.einsum("km,ptxkl,ln->ptxmn", Dw, C.astype(np.float32), Dw, optimize=True)
-    out = np.zeros_like(xp)
-    for py in range(2):
-        for px in range(2):
-            sub = T[:, py::2, px::2]
-            ny, nx = sub.shape[1], sub.shape[2]
-            blk = sub.transpose(0, 1, 3, 2, 4).reshape(x.shape[0], ny * n, nx * n)
-            out[:, py * h:py * h + ny * n, px * h:px * h + nx * n] += blk
-    return out[:, h:h + H, h:h + W].reshape(lead + (H, W)).astype(np.float32)
+    Dw = dct_window_matrix(n)
+    C = dct_core(dct_coefficients(x, n), threshold, mode)
+    R = mm_right(mm_left(np.ascontiguousarray(Dw.T), C), Dw)
+    return dct_overlap_add(R, H, W, n).reshape(lead + (H, W)).astype(np.float32)
+
+
+def dct_flip_mask(img, threshold, eps, n=16):
+    """Pixels whose hard-coring result depends on a coefficient within `eps`
+    of the threshold: any non-DC coefficient of any tile covering the pixel
+    with ||c| - threshold| <= eps.  An implementation whose forward
+    coefficients are within eps of these can decide such a coefficient
+    either way; every other pixel has an unambiguous result."""
+    x = np.asarray(img, np.float32)
+    H, W = x.shape[-2:]
+    C = dct_coefficients(x, n)
+    near = np.abs(np.abs(C) - np.float32(threshold)) <= eps
+    near[..., 0, 0] = False
+    tile = near.any(axis=(-1, -2))  # (P, ty, tx)
+    h = n // 2
+    P, ty, tx = tile.shape
+    m = np.zeros((P, H + 2 * h, W + 2 * h), bool)
+    for p, i, j in zip(*np.nonzero(tile)):
+        m[p, h * i:h * i + n, h * j:h * j + n] = True
+    return m[:, h:h + H, h:h + W].reshape(x.shape[:-2] + (H, W))

@@ -163,3 +163,34 @@ def test_lanczos_weights_properties():
     # known interior values (SURVEY appendix A probe)
     np.testing.assert_allclose(w[100, :6], [0.0037, 0.0151, -0.0340, -0.0666, 0.1355, 0.4464],
                                atol=1e-4)
+
+
+def test_dct_oracle_pinned_to_reference_wmma_programs(G, J):
+    """DCT-16 denoise: the oracle's four 16x16x16 products per tile are
+    bit-identical to wmma_mma programs run by the reference interpreter in
+    strict mode (oracle/make_golden.py: mm_program), and so is the whole
+    denoise (hard, soft, threshold 0) of a 2x40x56 bf16 image."""
+    img = G["dct_img"]
+    assert J["dct"]["strict"] and J["dct"]["wmma_shape"] == [16, 16, 16]
+    assert same_bits(pipelines_ref.dct_window_matrix(), G["dct_Dw"])
+    assert same_bits(pipelines_ref.dct_coefficients(img), G["dct_coeffs"])
+    thr = J["dct"]["threshold"]
+    assert same_bits(pipelines_ref.dct_denoise(img, thr, "hard"), G["dct_out_hard"])
+    assert same_bits(pipelines_ref.dct_denoise(img, thr, "soft"), G["dct_out_soft"])
+    assert same_bits(pipelines_ref.dct_denoise(img, 0.0, "soft"), G["dct_out_zero"])
+
+
+def test_dct_flip_mask():
+    rng = np.random.default_rng(3)
+    yy, xx = np.mgrid[0:96, 0:128]
+    img = np.clip(0.5 + 0.4 * np.sin(xx / 17.0) * np.cos(yy / 23.0)
+                  + rng.normal(0, 0.05, (1, 96, 128)), 0, 1).astype(np.float32)
+    C = pipelines_ref.dct_coefficients(img)
+    m0 = pipelines_ref.dct_flip_mask(img, 0.15, 0.0)
+    m1 = pipelines_ref.dct_flip_mask(img, 0.15, 3e-3)
+    assert m0.shape == img.shape and m0.sum() <= m1.sum()
+    assert m1.any() and not m1.all()
+    # a coefficient exactly at the threshold flags its tile's 16x16 footprint
+    c = abs(float(C[0, 2, 3, 4, 5]))
+    m = pipelines_ref.dct_flip_mask(img, c, 0.0)
+    assert m[0, 8:24, 16:32].all()
