@@ -26,13 +26,18 @@
 //   S7  (SS f16, N=128)   D4[r][c] += Σ_f T_gᵀ[r][f] B7[f][c]   (both g accumulate)
 //   E4  D4 (lane = band row) -> output block, one TMA store
 //
-// Precision: the forward chain decides coring, so its f32 intermediates
-// travel as bf16 hi/lo pairs (~16 mantissa bits; kind::tf32 does not accept
-// an MN-major A from shared memory on sm_100a — it silently yields zeros, see
-// ts_probe_mma amode 3).  The inverse chain is linear and only has to meet
-// the output tolerance: one fp16 operand per step (11 bits; max error ~1e-3
-// against the f32 oracle, tools/sim_dct_precision.py), half the MMAs and
-// conversions of hi/lo.
+// Precision: the forward chain decides coring, so it is f32-accurate up to
+// ~2^-22: S1 multiplies the (bf16-exact) image by a 3-term bf16 expansion of
+// Dw (hi + mid + lo, residual < 2^-24), C1 splits D1 into fp16 hi/lo pairs
+// (22 significant bits) and S3 runs hi·hi + lo·hi + hi·lo in kind::f16
+// (Dwᵀ also as fp16 hi/lo); every MMA accumulates in f32.  Worst-case bound
+// on a coefficient for inputs in [0, 1]: 5e-5 (K3); measured
+// ~1e-6.  kind::tf32 is no way out: it does not accept an MN-major A from
+// shared memory on sm_100a (it silently yields zeros).  The inverse chain
+// is linear and only has to meet the output tolerance: one fp16 operand per
+// step (11 bits; max error ~1e-3 against the f32 oracle,
+// tools/sim_dct_precision.py).  fp16 intermediates bound the input range:
+// |x| <= 2048 (coefficients stay below the fp16 maximum).
 //
 // Clamp-to-edge: TMA zero-fills samples outside the image; for bands on an
 // image border the loader warp replicates the edge row / column into the 8
@@ -41,6 +46,7 @@
 // variants.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -67,7 +73,7 @@ namespace dct {
 //   B3       : Dwᵀ as the S3 B operand (K = sample, N = freq), hi + lo
 //   B5       : Dw f32 (K = freq, N = sample) for S5
 constexpr uint32_t kStripBytes = 8192;
-constexpr uint32_t kCS7 = 2 * kStripBytes;
+constexpr uint32_t kCS7 = 3 * kStripBytes;  // S1 strip: hi, mid, lo
 constexpr uint32_t kCB3 = kCS7 + 7936;
 constexpr uint32_t kCB5 = kCB3 + 1024;
 constexpr uint32_t kConstBytes = kCB5 + 1024;
@@ -186,14 +192,13 @@ __device__ __forceinline__ uint32_t sw_off(int row, int col) {
   return (col >> 6) * 16384u + row * 128u + ((((col & 63) >> 3) ^ (row & 7)) << 4) + (col & 7) * 2u;
 }
 
-// bf16 hi/lo split of a pair with ONE conversion: hi rounds to nearest
-// (F2FP); the residuals a - hi are exact in f32 and are truncated to bf16 by
-// a byte permute (|lo| < 2^-8 |a|, so truncation costs < 2^-16 |a|).  The
-// conversion pipe, not TMEM, bounds the DCT epilogues.
+// fp16 hi/lo split of a pair: hi = RNE(a), lo = RNE(a - hi).  |a - hi - lo|
+// <= 2^-22 |a| (+ 2^-25 in the subnormal range), i.e. ~22 significant bits
+// — the forward chain's operand precision (its MMAs accumulate in f32).
 __device__ __forceinline__ uint32_t hi_lo(float a, float b, uint32_t* lo) {
-  const uint32_t h = pack_bf16x2(a, b);  // a -> low half, b -> high half (RNE)
-  const float la = a - __uint_as_float(h << 16), lb = b - __uint_as_float(h & 0xFFFF0000u);
-  *lo = __byte_perm(__float_as_uint(la), __float_as_uint(lb), 0x7632);
+  const uint32_t h = pack_f16x2(a, b);  // a -> low half (RNE)
+  const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+  *lo = pack_f16x2(a - hf.x, b - hf.y);
   return h;
 }
 
@@ -337,7 +342,6 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t id128 = make_idesc(kFmtBF16, 128, BW, /*A K-major*/ 0, /*B MN*/ 1);
-    const uint32_t id16 = make_idesc(kFmtBF16, 128, 16, 0, 0);
     const uint32_t id16h = make_idesc(kFmtF16, 128, 16, 0, 0);
     const uint32_t id128h = make_idesc(kFmtF16, 128, BW, 0, 1);
     const uint64_t a_tmpl = make_sdesc(0u, 128u, 256u, kSwizzleNone);
@@ -358,9 +362,11 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       for (int m = 4 * g; m < 5 + 3 * g; ++m) {
         const uint32_t so = 256u - 64u * m + 256u * g;  // strip window, 16-byte units
         const uint32_t acc = m > 4 * g ? 1u : 0u;
-        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + so), bx + 128u * m, id128, acc);
+        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + so), bx + 128u * m, id128, acc);  // hi
         mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + kStripBytes / 16 + so), bx + 128u * m, id128,
                          1u);
+        mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + 2 * kStripBytes / 16 + so), bx + 128u * m,
+                         id128, 1u);
       }
       mma_commit_elect(s1done);  // before any later S7: C1 must not wait for it
       if (g == 1) mma_commit_elect(&xempty[s]);
@@ -386,9 +392,9 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
           for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j) {
             const uint32_t pc = 8u * j + 4u * q;  // packed column of the tile's first sample
             const uint32_t d = tmem + kTD2 + 16u * (G::kNq0 * q + j);
-            mma_f16_ts_elect(d, tmem + kTD1 + pc, b3, id16, 0u);
-            mma_f16_ts_elect(d, tmem + kTD1 + BW / 2 + pc, b3, id16, 1u);
-            mma_f16_ts_elect(d, tmem + kTD1 + pc, b3 + 32u, id16, 1u);
+            mma_f16_ts_elect(d, tmem + kTD1 + pc, b3, id16h, 0u);
+            mma_f16_ts_elect(d, tmem + kTD1 + BW / 2 + pc, b3, id16h, 1u);
+            mma_f16_ts_elect(d, tmem + kTD1 + pc, b3 + 32u, id16h, 1u);
           }
           mma_commit_elect(&s3done[q]);  // E2 cores column phase q while S3 runs q + 1
         }
@@ -666,35 +672,47 @@ static void build_consts(uint8_t* out) {
     if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
     return static_cast<uint16_t>(sign | h);
   };
-  // K-major no-swizzle core matrices, 16 K: element (row n, k) of a bf16 operand
-  auto put16 = [&](uint8_t* dst, int n, int kk, double v, int lo) {
+  auto f16_val = [](uint16_t h) {
+    const double m = (h & 0x3FF), e = (h >> 10) & 0x1F;
+    const double v = e == 0 ? m * std::ldexp(1.0, -24) : (1024.0 + m) * std::ldexp(1.0, e - 25);
+    return (h & 0x8000) ? -v : v;
+  };
+  // K-major no-swizzle core matrices, 16 K: element (row n, k) of a bf16
+  // operand; term 0/1/2 = hi / mid / lo of the 3-term bf16 expansion
+  auto put16 = [&](uint8_t* dst, int n, int kk, double v, int term) {
     uint16_t h = bf16_bits(v);
-    if (lo) h = bf16_bits(v - bf16_val(h));
+    for (int t = 0; t < term; ++t) {
+      v -= bf16_val(h);
+      h = bf16_bits(v);
+    }
     std::memcpy(dst + (n / 8) * 256 + (kk / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2, &h, 2);
   };
-  auto put16h = [&](uint8_t* dst, int n, int kk, double v) {
-    const uint16_t h = f16_bits(v);
+  auto put16h = [&](uint8_t* dst, int n, int kk, double v, int lo = 0) {
+    uint16_t h = f16_bits(v);
+    if (lo) h = f16_bits(v - f16_val(h));
     std::memcpy(dst + (n / 8) * 256 + (kk / 8) * 128 + (n % 8) * 16 + (kk % 8) * 2, &h, 2);
   };
   // S1 strip: the 48-row block of K-step m at strip rows 112 + 16 d + k
   // (d = t - 2m + 1, tile t's frequency k; K = band row 16m + kk, i.e. tile
   // row kk + 8 - 8d); K-step m of group g reads the window starting at
   // strip row 128 - 32 m + 128 g, so that tile t lands on lane 16 (t - 8g) + k.
-  for (int lo = 0; lo < 2; ++lo)
+  // (the image is exact in bf16, so three bf16 terms of Dw make S1 f32-accurate)
+  for (int term = 0; term < 3; ++term)
     for (int d = 0; d < 3; ++d)
       for (int k = 0; k < 16; ++k)
         for (int kk = 0; kk < 16; ++kk) {
           const int r = kk + 8 - 8 * d;
-          if (r >= 0 && r < 16) put16(out + lo * dct::kStripBytes, 112 + 16 * d + k, kk, D[k][r], lo);
+          if (r >= 0 && r < 16)
+            put16(out + term * dct::kStripBytes, 112 + 16 * d + k, kk, D[k][r], term);
         }
   // S7 strip (fp16): A7[r][kk] = Dw[kk][r - 16k - 8p] at g = r + 120 - 16k - 8p
   for (int m = 0; m < 16; ++m)
     for (int kk = 0; kk < 16; ++kk) put16h(out + dct::kCS7, 120 + m, kk, D[kk][m]);
-  // B3[K = sample c][N = freq l] = Dw[l][c]: hi, lo
+  // B3[K = sample c][N = freq l] = Dw[l][c]: fp16 hi, lo
   for (int l = 0; l < 16; ++l)
     for (int c = 0; c < 16; ++c) {
-      put16(out + dct::kCB3, l, c, D[l][c], 0);
-      put16(out + dct::kCB3 + 512, l, c, D[l][c], 1);
+      put16h(out + dct::kCB3, l, c, D[l][c], 0);
+      put16h(out + dct::kCB3 + 512, l, c, D[l][c], 1);
     }
   // B5[K = freq l][N = sample c] = Dw[l][c] (fp16)
   for (int c = 0; c < 16; ++c)

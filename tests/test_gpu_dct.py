@@ -1,16 +1,25 @@
 """DCT-16 denoise (config 4) against the CPU oracle.
 
-Soft coring is Lipschitz, so the north-star bound applies directly
-(max |gpu - oracle| <= 1e-2).  Hard coring (the paper's) is discontinuous:
-a coefficient within rounding distance of the threshold can be kept by one
-side and zeroed by the other, so for it the bound is checked on all but a
-tiny fraction of pixels, and the flips are bounded in size.
+The oracle's transform is pinned bitwise to wmma_mma programs run by the
+reference (tests/test_oracle_golden.py).  Soft coring is Lipschitz, so the
+north-star bound applies to every pixel (max |gpu - oracle| <= 1e-2).  Hard
+coring (the paper's) is discontinuous: a coefficient within the GPU forward
+chain's error of the threshold can be kept by one side and zeroed by the
+other.  The GPU's forward coefficients are within EPS_FWD of the oracle's
+(worst-case bound, K3), so every pixel must be within 1e-2 except
+pixels covered by a tile holding a coefficient within EPS_FWD of the
+threshold — a mask the oracle computes (pipelines_ref.dct_flip_mask).
 """
 
 import numpy as np
 import pytest
 
+from conftest import oracle_planes
 from oracle import pipelines_ref
+
+# the forward chain's stated worst-case coefficient error for inputs in
+# [0, 1] (3-term bf16 S1, fp16 hi/lo S3, f32 accumulation; K3)
+EPS_FWD = 1e-4
 
 pytestmark = pytest.mark.gpu
 
@@ -49,14 +58,26 @@ def test_soft_coring_matches_oracle(shape):
     assert np.abs(y - ref).max() <= 1e-2
 
 
-@pytest.mark.parametrize("shape", [(1, 232, 360), (1, 2160, 3840)])
-def test_hard_coring_matches_oracle_up_to_threshold_flips(shape):
+@pytest.mark.parametrize("shape", [(1, 232, 360), (3, 2160, 3840)])
+def test_hard_coring_matches_oracle_per_pixel(shape):
+    """Every pixel within 1e-2 except those whose tiles hold a coefficient
+    within EPS_FWD of the threshold (config c4: a full 3 x 2160 x 3840
+    frame)."""
     x = _noisy(shape, 3)
     y = _gpu(x, threshold=0.15, mode="hard")
-    ref = pipelines_ref.dct_denoise(x, 0.15, "hard")
+    ref = oracle_planes("dct_denoise", x, 0.15, "hard")
+    excused = oracle_planes("dct_flip_mask", x, 0.15, EPS_FWD)
     d = np.abs(y - ref)
-    assert (d > 1e-2).mean() < 1e-3, (d > 1e-2).mean()
-    assert d.max() < 0.1
+    bad = (d > 1e-2) & ~excused
+    assert not bad.any(), (int(bad.sum()), float(d[bad].max()))
+    assert excused.mean() < 2e-3, excused.mean()  # the excusal is rare
+
+
+def test_soft_coring_full_frame():
+    x = _noisy((3, 2160, 3840), 6)
+    y = _gpu(x, threshold=0.15, mode="soft")
+    ref = oracle_planes("dct_denoise", x, 0.15, "soft")
+    assert np.abs(y - ref).max() <= 1e-2
 
 
 def test_denoising_reduces_error():

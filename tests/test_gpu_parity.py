@@ -9,6 +9,7 @@ one frame (the oracle runs on the GPU box's CPU).
 import numpy as np
 import pytest
 
+from conftest import oracle_planes
 from oracle import pipelines_ref
 
 pytestmark = pytest.mark.gpu
@@ -90,6 +91,31 @@ def test_gaussian_8k_rows(taps):
     x = _img((1, 256, 7680), 40 + taps, smooth=True)
     y = _gpu(pipelines.gaussian_blur, x, taps=taps)
     ref = pipelines_ref.gaussian_blur(x, taps)
+    assert np.abs(y - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("taps", [9, 31])
+def test_gaussian_8k_full_frame(taps):
+    """Config c3 at its stated shape: one 3 x 4320 x 7680 bf16 frame, every
+    pixel against the oracle."""
+    from paper_2512_02371_b200 import pipelines
+    x = _img((3, 4320, 7680), 50 + taps, smooth=True)
+    y = _gpu(pipelines.gaussian_blur, x, taps=taps)  # bf16 out (the bench's output)
+    ref = oracle_planes("gaussian_blur", x, taps)
+    assert y.shape == ref.shape == (3, 4320, 7680)
+    assert np.abs(y - ref).max() <= TOL
+
+
+def test_resample_filter_4k_full_frame():
+    """Config c5 at its stated shape: one 3 x 2160 x 3840 frame -> 1080p
+    Lanczos-3 then the 9-tap Gaussian (one fused pass on the GPU; two
+    separate passes in the oracle)."""
+    from paper_2512_02371_b200 import pipelines
+    x = _img((3, 2160, 3840), 60)
+    y = _gpu(pipelines.resample_filter, x, out_h=1080, out_w=1920, taps=9)
+    mid = oracle_planes("resample", x, 1080, 1920)
+    ref = oracle_planes("gaussian_blur", mid, 9)
+    assert y.shape == ref.shape == (3, 1080, 1920)
     assert np.abs(y - ref).max() <= TOL
 
 
