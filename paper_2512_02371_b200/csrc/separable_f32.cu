@@ -12,17 +12,20 @@
 // bit-identical to the oracle's.
 //
 // Uniform axes only (first[o] = S*o + base and the same T taps for every
-// output: the exact-2x Lanczos-3 axis and the centred filters): one CTA per
-// 32 x 64 output tile stages its (S*31+T) x (S*63+T) input window with
-// 16-byte cp.async (per-column clamped 4-byte copies at image edges — the
-// reference's clamp-to-edge), runs the horizontal pass into a shared f32
-// buffer, then the vertical pass straight to global.  Taps live in
+// output: the exact-2x Lanczos-3 axis and the centred filters).  Persistent
+// CTAs walk 32 x 64 output tiles; a tile's (S*31+T) x (S*63+T) input window
+// arrives as ONE TMA box (pitch 4 mod 32 floats, zero-filled outside the
+// image; border tiles then replicate the edge rows / columns — the
+// reference's clamp-to-edge), the horizontal pass runs into a shared f32
+// buffer, and while the vertical pass writes this tile straight to global
+// the next tile's window is already in flight.  Taps live in
 // registers; each thread computes 4 consecutive outputs from one register
 // window (float4 shared loads of S*3+T inputs instead of 4*T scalar ones);
 // the vertical pass takes column pairs through packed f32x2 FMAs (FFMA2).
 // With TS_F32_EXACT the taps are multiplied and added separately (the
 // reference's rounding, bit-exact); without it they are fused multiply-adds
 // (one rounding per tap fewer, ~half the FP32 instructions).
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -30,16 +33,14 @@
 #include "sm100.cuh"
 
 namespace tsb {
+ts_status encode_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* ptr,
+                         int64_t d0, int64_t d1, int64_t d2, int64_t stride1_elems,
+                         int64_t stride2_elems, int box0, int box1, CUtensorMapSwizzle swz);
+int sm_count_current();
+
 namespace {
 
 constexpr int kTR = 32, kTC = 64, kThreads = 256, kR = 4, kRH = 8;
-
-__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
 
 // Window geometry of one tile for (stride S, taps T, column misalignment OFF):
 // the staged window starts at the 16-byte-aligned column c0 - OFF.
@@ -58,6 +59,7 @@ struct Geo {
   static constexpr int NVH = S * (kRH - 1) + T;            // taps of kRH horizontal outputs
   static constexpr int NVA = (OFF + NVH + 3) & ~3;         // as whole float4s
   static constexpr int smem = 4 * (SR * WP + SR * HP);
+  static_assert(WP <= 256 && SR <= 256, "one TMA box per window");
 };
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // FFMA2
@@ -72,41 +74,42 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // FFMA
 
 template <int S, int T, int OFF, bool BF16, bool EXACT>
 __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel(
-    const float* __restrict__ in, int H, int W, int64_t irs, int64_t ips, int vec_ok,
+    const __grid_constant__ CUtensorMap tm_in, int H, int W, int ntx, int nty, int ntiles,
     void* __restrict__ out, int OH, int OW, int64_t ors, int64_t ops, int rbase, int cbase,
     const float* __restrict__ rw, const float* __restrict__ cw, EpiK ek) {
   using G = Geo<S, T, OFF>;
-  extern __shared__ __align__(16) float sm[];
-  float* win = sm;                  // SR x WP  input window (f32, as loaded)
+  extern __shared__ __align__(128) float sm[];
+  float* win = sm;                  // SR x WP  input window (f32, one TMA box)
   float* hb = win + G::SR * G::WP;  // SR x HP  horizontal pass
-
-  const int p = blockIdx.z, or0 = blockIdx.y * kTR, oc0 = blockIdx.x * kTC;
-  const int r0 = S * or0 + rbase, c0a = S * oc0 + cbase - OFF;
-  const float* src = in + p * ips;
+  __shared__ __align__(8) uint64_t full;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  (void)lane;
+  (void)warp;
 
-  const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(win));
-  // the window streams in as two cp.async groups (top / bottom rows): the
-  // horizontal pass over the top rows overlaps the bottom rows' loads
-  constexpr int QC = G::SCA / 4;  // 16-byte chunks per window row
-  constexpr int RH = G::SR / 2;
-  auto stage = [&](int lo, int hi) {
-    for (int idx = lo * QC + tid; idx < hi * QC; idx += kThreads) {
-      const int r = idx / QC, q = idx - r * QC;
-      const float* row = src + static_cast<int64_t>(min(max(r0 + r, 0), H - 1)) * irs;
-      const int gc = c0a + 4 * q;
-      const uint32_t d = wbase + 4u * (r * G::WP + 4 * q);
-      if (vec_ok && gc >= 0 && gc + 3 < W) {
-        cp_async16(d, row + gc);
-      } else {  // image edge: clamp each column (the reference's clamp-to-edge)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) cp_async4(d + 4u * e, row + min(max(gc + e, 0), W - 1));
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+  // tile t -> (plane, output row block, output column block)
+  auto coords = [&](int t, int& p, int& or0, int& oc0) {
+    oc0 = (t % ntx) * kTC;
+    const int rest = t / ntx;
+    or0 = (rest % nty) * kTR;
+    p = rest / nty;
   };
-  stage(0, RH);
-  stage(RH, G::SR);
+  // the whole (SR x WP) window as one TMA box at (column S*oc0 + cbase - OFF,
+  // row S*or0 + rbase); samples outside the image arrive as zeros
+  auto issue = [&](int t) {
+    int p, or0, oc0;
+    coords(t, p, or0, oc0);
+    fence_proxy_async_smem();  // this CTA's generic writes (edge fix-up) before the async overwrite
+    mbar_arrive_expect_tx(&full, G::SR * G::WP * 4);
+    tma_load_3d(win, &tm_in, &full, S * oc0 + cbase - OFF, S * or0 + rbase, p);
+  };
+  if (tid == 0) {
+    mbar_init(&full, 1);
+    fence_barrier_init();
+    prefetch_tmap(&tm_in);
+    if (static_cast<int>(blockIdx.x) < ntiles) issue(blockIdx.x);
+  }
+  __syncthreads();
+
   // every output of a uniform axis has the same taps: hold them in registers
   float wc[T];
   float2 wr2[T];  // row taps duplicated for the packed column-pair FMAs
@@ -121,6 +124,11 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
   for (int i = 0; i < T / 2; ++i)
     wcp[i] = make_float2(wc[min((OFF & 1) + 2 * i, T - 1)], wc[min((OFF & 1) + 2 * i + 1, T - 1)]);
 
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  int p, or0, oc0;
+  coords(tile, p, or0, oc0);
+  const int r0 = S * or0 + rbase, c0a = S * oc0 + cbase - OFF;
   // horizontal pass: task = (group g of kRH output columns, window row r); the
   // lanes of a warp walk consecutive rows
   auto hpass = [&](int lo, int hi) {
@@ -169,13 +177,30 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
           make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
   }
   };
-  asm volatile("cp.async.wait_group 1;" ::: "memory");
-  __syncthreads();
-  hpass(0, RH);
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  hpass(RH, G::SR);
-  __syncthreads();
+  mbar_wait(&full, it & 1);
+  if (r0 < 0 || r0 + G::SR > H || c0a < 0 || c0a + G::SCA > W) {
+    // clamp-to-edge (the reference's boundary policy): replicate the edge
+    // rows, then the edge columns, over the zero-filled samples
+    for (int r = 0; r < G::SR; ++r) {
+      const int gr = r0 + r;
+      if (gr >= 0 && gr < H) continue;
+      const int sr = min(max(gr, 0), H - 1) - r0;
+      for (int q = tid; q < G::SCA; q += kThreads) win[r * G::WP + q] = win[sr * G::WP + q];
+    }
+    __syncthreads();
+    const int nl = min(max(-c0a, 0), G::SCA);            // columns left of the image
+    const int rb0 = max(min(W - c0a, G::SCA), nl);       // first column right of it
+    const int nb = nl + (G::SCA - rb0);
+    for (int idx = tid; idx < G::SR * nb; idx += kThreads) {
+      const int r = idx / nb, j = idx - r * nb;
+      const int q = j < nl ? j : rb0 + (j - nl);
+      win[r * G::WP + q] = win[r * G::WP + (min(max(c0a + q, 0), W - 1) - c0a)];
+    }
+    __syncthreads();
+  }
+  hpass(0, G::SR);
+  __syncthreads();  // window consumed: stage the next tile while the vertical pass runs
+  if (tid == 0 && tile + static_cast<int>(gridDim.x) < ntiles) issue(tile + gridDim.x);
 
   // vertical pass: task = (group g of kR output rows, column pair j, j+1);
   // the lanes walk consecutive column pairs (one float2 per window row), and
@@ -214,6 +239,8 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
       }
     }
   }
+  __syncthreads();  // hb consumed before the next tile's horizontal pass
+  }
 }
 
 template <int S, int T, int OFF, bool BF16, bool EXACT>
@@ -231,9 +258,25 @@ ts_status launch_f32(int planes, const float* in, int H, int W, int64_t irs, int
     if (attr != cudaSuccess) return cuda_error(attr, "separable_f32: smem attribute");
     attr_done[dev].store(true);
   }
-  const int vec_ok = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && irs % 4 == 0 && ips % 4 == 0;
-  dim3 grid((OW + kTC - 1) / kTC, (OH + kTR - 1) / kTR, planes);
-  fn<<<grid, kThreads, smem, st>>>(in, H, W, irs, ips, vec_ok, out, OH, OW, ors, ops, rb, cb, rw,
+  if (reinterpret_cast<uintptr_t>(in) % 16 || irs % 4 || ips % 4)
+    return set_error(TS_ERR_UNSUPPORTED,
+                     "separable_f32: TMA needs a 16-byte aligned image with row and plane "
+                     "strides that are multiples of 4 floats");
+  CUtensorMap tm;
+  ts_status ts = encode_tmap_3d(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in, W, H, planes, irs, ips,
+                                Geo<S, T, OFF>::WP, Geo<S, T, OFF>::SR,
+                                CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (ts != TS_OK) return ts;
+  const int ntx = (OW + kTC - 1) / kTC, nty = (OH + kTR - 1) / kTR;
+  const int64_t ntiles64 = static_cast<int64_t>(ntx) * nty * planes;
+  if (ntiles64 > (1 << 30)) return set_error(TS_ERR_UNSUPPORTED, "separable_f32: too many tiles");
+  const int ntiles = static_cast<int>(ntiles64);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem);
+  // persistent CTAs: each stages its next tile while it runs this one's vertical pass
+  const int slots = (per_sm > 0 ? per_sm : 1) * sm_count_current();
+  const int grid = ntiles < slots ? ntiles : slots;
+  fn<<<grid, kThreads, smem, st>>>(tm, H, W, ntx, nty, ntiles, out, OH, OW, ors, ops, rb, cb, rw,
                                    cw, ek);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "separable_f32 launch");
