@@ -134,17 +134,23 @@ def _run_f32(x, ra, ca, out_dtype, ep, stream):
     torch = _torch()
     H, W = x.shape[-2], x.shape[-1]
     P = math.prod(x.shape[:-2]) if x.dim() > 2 else 1
-    if W % 4 or x.data_ptr() % 16:  # the window is one TMA box: 16-byte rows
-        return None
+    lead = x.shape[:-2]
+    rs = W
+    if W % 4 or x.data_ptr() % 16:
+        # the window is one TMA box: rows must start on 16 bytes -> a pitched copy
+        rs = -(-W // 4) * 4
+        xp = torch.empty((P, H, rs), dtype=torch.float32, device=x.device)
+        xp[:, :, :W] = x.reshape(P, H, W)
+        x = xp
     oh, ow = ra.n_out, ca.n_out
     out = torch.empty((P, oh, ow), dtype=out_dtype, device=x.device)
     ts_out = _lib.TS_BF16 if out_dtype == torch.bfloat16 else _lib.TS_F32
     wr, wc = ra.device_weights(), ca.device_weights()
     _lib.check(_lib.load().ts_separable_f32_ep(
-        P, x.data_ptr(), H, W, W, W * H, ur[0], ur[1], ur[2], wr.data_ptr(), oh, uc[2],
+        P, x.data_ptr(), H, W, rs, rs * H, ur[0], ur[1], ur[2], wr.data_ptr(), oh, uc[2],
         wc.data_ptr(), ow, out.data_ptr(), ow, ow * oh, ts_out, 1 if F32_EXACT else 0,
         None if ep is None else _ep_ptr(ep), stream), "ts_separable_f32_ep")
-    return out.reshape(*x.shape[:-2], oh, ow)
+    return out.reshape(*lead, oh, ow)
 
 
 def _run(x, ra, ca, out_dtype, ep=None):
