@@ -72,11 +72,17 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // FFMA
   return *reinterpret_cast<float2*>(&d);
 }
 
-template <int S, int T, int OFF, bool BF16, bool EXACT>
+// (column block, row block, plane) of a tile, advanced by the grid stride
+// with carries instead of a runtime division per tile
+struct TileIdx {
+  int tx, ty, p;
+};
+
+template <int S, int T, int OFF, bool BF16, bool EXACT, bool EPI>
 __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel(
-    const __grid_constant__ CUtensorMap tm_in, int H, int W, int ntx, int nty, int ntiles,
-    void* __restrict__ out, int OH, int OW, int64_t ors, int64_t ops, int rbase, int cbase,
-    const float* __restrict__ rw, const float* __restrict__ cw, EpiK ek) {
+    const __grid_constant__ CUtensorMap tm_in, int H, int W, int ntx, int nty, int planes,
+    void* __restrict__ out, int OH, int OW, int64_t ors, int64_t ops, int vec2, int rbase,
+    int cbase, const float* __restrict__ rw, const float* __restrict__ cw, EpiK ek) {
   using G = Geo<S, T, OFF>;
   extern __shared__ __align__(128) float sm[];
   float* win = sm;                  // SR x WP  input window (f32, one TMA box)
@@ -86,27 +92,36 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
   (void)lane;
   (void)warp;
 
-  // tile t -> (plane, output row block, output column block)
-  auto coords = [&](int t, int& p, int& or0, int& oc0) {
-    oc0 = (t % ntx) * kTC;
+  auto decompose = [&](int t) {
+    TileIdx c;
+    c.tx = t % ntx;
     const int rest = t / ntx;
-    or0 = (rest % nty) * kTR;
-    p = rest / nty;
+    c.ty = rest % nty;
+    c.p = rest / nty;
+    return c;
+  };
+  const TileIdx step = decompose(gridDim.x);
+  auto advance = [&](TileIdx c) {
+    c.tx += step.tx;
+    if (c.tx >= ntx) c.tx -= ntx, ++c.ty;
+    c.ty += step.ty;
+    if (c.ty >= nty) c.ty -= nty, ++c.p;
+    c.p += step.p;
+    return c;
   };
   // the whole (SR x WP) window as one TMA box at (column S*oc0 + cbase - OFF,
   // row S*or0 + rbase); samples outside the image arrive as zeros
-  auto issue = [&](int t) {
-    int p, or0, oc0;
-    coords(t, p, or0, oc0);
+  auto issue = [&](const TileIdx& c) {
     fence_proxy_async_smem();  // this CTA's generic writes (edge fix-up) before the async overwrite
     mbar_arrive_expect_tx(&full, G::SR * G::WP * 4);
-    tma_load_3d(win, &tm_in, &full, S * oc0 + cbase - OFF, S * or0 + rbase, p);
+    tma_load_3d(win, &tm_in, &full, S * kTC * c.tx + cbase - OFF, S * kTR * c.ty + rbase, c.p);
   };
+  TileIdx cur = decompose(blockIdx.x);
   if (tid == 0) {
     mbar_init(&full, 1);
     fence_barrier_init();
     prefetch_tmap(&tm_in);
-    if (static_cast<int>(blockIdx.x) < ntiles) issue(blockIdx.x);
+    if (cur.p < planes) issue(cur);
   }
   __syncthreads();
 
@@ -125,15 +140,14 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
     wcp[i] = make_float2(wc[min((OFF & 1) + 2 * i, T - 1)], wc[min((OFF & 1) + 2 * i + 1, T - 1)]);
 
   int it = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-  int p, or0, oc0;
-  coords(tile, p, or0, oc0);
+  for (; cur.p < planes; cur = advance(cur), ++it) {
+  const int p = cur.p, or0 = kTR * cur.ty, oc0 = kTC * cur.tx;
   const int r0 = S * or0 + rbase, c0a = S * oc0 + cbase - OFF;
   // horizontal pass: task = (group g of kRH output columns, window row r); the
   // lanes of a warp walk consecutive rows
-  auto hpass = [&](int lo, int hi) {
-  for (int task = tid; task < (hi - lo) * (kTC / kRH); task += kThreads) {
-    const int g = task / (hi - lo), r = lo + task - g * (hi - lo);
+  auto hpass = [&]() {
+  for (int task = tid; task < G::SR * (kTC / kRH); task += kThreads) {
+    const int g = task / G::SR, r = task - g * G::SR;
     const float4* x = reinterpret_cast<const float4*>(win + r * G::WP + S * kRH * g);
     float v[G::NVA];
 #pragma unroll
@@ -181,11 +195,13 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
   if (r0 < 0 || r0 + G::SR > H || c0a < 0 || c0a + G::SCA > W) {
     // clamp-to-edge (the reference's boundary policy): replicate the edge
     // rows, then the edge columns, over the zero-filled samples
-    for (int r = 0; r < G::SR; ++r) {
-      const int gr = r0 + r;
-      if (gr >= 0 && gr < H) continue;
-      const int sr = min(max(gr, 0), H - 1) - r0;
-      for (int q = tid; q < G::SCA; q += kThreads) win[r * G::WP + q] = win[sr * G::WP + q];
+    const int top = min(max(-r0, 0), G::SR);          // window rows above the image
+    const int bot = max(min(H - r0, G::SR), top);     // first window row below it
+    const int nr = top + (G::SR - bot);
+    for (int idx = tid; idx < nr * G::SCA; idx += kThreads) {
+      const int i = idx / G::SCA, q = idx - i * G::SCA;
+      const int r = i < top ? i : bot + (i - top);
+      win[r * G::WP + q] = win[(i < top ? -r0 : H - 1 - r0) * G::WP + q];
     }
     __syncthreads();
     const int nl = min(max(-c0a, 0), G::SCA);            // columns left of the image
@@ -198,9 +214,12 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
     }
     __syncthreads();
   }
-  hpass(0, G::SR);
+  hpass();
   __syncthreads();  // window consumed: stage the next tile while the vertical pass runs
-  if (tid == 0 && tile + static_cast<int>(gridDim.x) < ntiles) issue(tile + gridDim.x);
+  if (tid == 0) {
+    const TileIdx nxt = advance(cur);
+    if (nxt.p < planes) issue(nxt);
+  }
 
   // vertical pass: task = (group g of kR output rows, column pair j, j+1);
   // the lanes walk consecutive column pairs (one float2 per window row), and
@@ -226,15 +245,28 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
       }
       const int orow = or0 + kR * g + k;
       if (orow < OH) {
-        const float y0 = epi_f32(ek, __fadd_rn(acc.x, 0.0f));
-        const float y1 = epi_f32(ek, __fadd_rn(acc.y, 0.0f));
+        float y0 = __fadd_rn(acc.x, 0.0f), y1 = __fadd_rn(acc.y, 0.0f);
+        if constexpr (EPI) {
+          y0 = epi_f32(ek, y0);
+          y1 = epi_f32(ek, y1);
+        }
         const int64_t o = p * ops + orow * ors + oc;
         if constexpr (BF16) {
-          if (oc < OW) static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(y0);
-          if (oc + 1 < OW) static_cast<__nv_bfloat16*>(out)[o + 1] = __float2bfloat16_rn(y1);
+          __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(out) + o;
+          if (vec2 && oc + 1 < OW) {
+            *reinterpret_cast<uint32_t*>(ob) = pack_bf16x2(y0, y1);
+          } else {
+            if (oc < OW) ob[0] = __float2bfloat16_rn(y0);
+            if (oc + 1 < OW) ob[1] = __float2bfloat16_rn(y1);
+          }
         } else {
-          if (oc < OW) static_cast<float*>(out)[o] = y0;
-          if (oc + 1 < OW) static_cast<float*>(out)[o + 1] = y1;
+          float* of = static_cast<float*>(out) + o;
+          if (vec2 && oc + 1 < OW) {
+            *reinterpret_cast<float2*>(of) = make_float2(y0, y1);
+          } else {
+            if (oc < OW) of[0] = y0;
+            if (oc + 1 < OW) of[1] = y1;
+          }
         }
       }
     }
@@ -243,12 +275,12 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
   }
 }
 
-template <int S, int T, int OFF, bool BF16, bool EXACT>
+template <int S, int T, int OFF, bool BF16, bool EXACT, bool EPI>
 ts_status launch_f32(int planes, const float* in, int H, int W, int64_t irs, int64_t ips, int rb,
                      const float* rw, int OH, int cb, const float* cw, int OW, void* out,
                      int64_t ors, int64_t ops, const EpiK& ek, cudaStream_t st) {
   constexpr int smem = Geo<S, T, OFF>::smem;
-  auto fn = separable_f32_kernel<S, T, OFF, BF16, EXACT>;
+  auto fn = separable_f32_kernel<S, T, OFF, BF16, EXACT, EPI>;
   static std::atomic<bool> attr_done[64] = {};  // the attribute is per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -276,23 +308,37 @@ ts_status launch_f32(int planes, const float* in, int H, int W, int64_t irs, int
   // persistent CTAs: each stages its next tile while it runs this one's vertical pass
   const int slots = (per_sm > 0 ? per_sm : 1) * sm_count_current();
   const int grid = ntiles < slots ? ntiles : slots;
-  fn<<<grid, kThreads, smem, st>>>(tm, H, W, ntx, nty, ntiles, out, OH, OW, ors, ops, rb, cb, rw,
-                                   cw, ek);
+  // paired stores need 2-element aligned rows (4 B bf16 pairs / 8 B f32 pairs)
+  const int vec2 = ors % 2 == 0 && ops % 2 == 0 &&
+                   reinterpret_cast<uintptr_t>(out) % (BF16 ? 4 : 8) == 0;
+  fn<<<grid, kThreads, smem, st>>>(tm, H, W, ntx, nty, planes, out, OH, OW, ors, ops, vec2, rb, cb,
+                                   rw, cw, ek);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "separable_f32 launch");
 }
 
-template <int S, int T, int OFF>
-ts_status launch_f32_any(bool bf, bool exact, int planes, const float* in, int H, int W,
+template <int S, int T, int OFF, bool EPI>
+ts_status launch_f32_epi(bool bf, bool exact, int planes, const float* in, int H, int W,
                          int64_t irs, int64_t ips, int rb, const float* rw, int OH, int cb,
                          const float* cw, int OW, void* out, int64_t ors, int64_t ops,
                          const EpiK& ek, cudaStream_t st) {
 #define TS_F32_ARGS planes, in, H, W, irs, ips, rb, rw, OH, cb, cw, OW, out, ors, ops, ek, st
-  if (bf) return exact ? launch_f32<S, T, OFF, true, true>(TS_F32_ARGS)
-                       : launch_f32<S, T, OFF, true, false>(TS_F32_ARGS);
-  return exact ? launch_f32<S, T, OFF, false, true>(TS_F32_ARGS)
-               : launch_f32<S, T, OFF, false, false>(TS_F32_ARGS);
+  if (bf) return exact ? launch_f32<S, T, OFF, true, true, EPI>(TS_F32_ARGS)
+                       : launch_f32<S, T, OFF, true, false, EPI>(TS_F32_ARGS);
+  return exact ? launch_f32<S, T, OFF, false, true, EPI>(TS_F32_ARGS)
+               : launch_f32<S, T, OFF, false, false, EPI>(TS_F32_ARGS);
 #undef TS_F32_ARGS
+}
+
+template <int S, int T, int OFF>
+ts_status launch_f32_any(bool epi, bool bf, bool exact, int planes, const float* in, int H, int W,
+                         int64_t irs, int64_t ips, int rb, const float* rw, int OH, int cb,
+                         const float* cw, int OW, void* out, int64_t ors, int64_t ops,
+                         const EpiK& ek, cudaStream_t st) {
+  return epi ? launch_f32_epi<S, T, OFF, true>(bf, exact, planes, in, H, W, irs, ips, rb, rw, OH,
+                                               cb, cw, OW, out, ors, ops, ek, st)
+             : launch_f32_epi<S, T, OFF, false>(bf, exact, planes, in, H, W, irs, ips, rb, rw, OH,
+                                                cb, cw, OW, out, ors, ops, ek, st);
 }
 
 }  // namespace
@@ -327,7 +373,7 @@ extern "C" ts_status ts_separable_f32_ep(int planes, const float* in, int in_h, 
   const int off = col_base & 3;  // misalignment of every tile's first column
 #define TS_F32_CASE(S_, T_, OFF_)                                                                \
   if (stride == S_ && taps == T_ && off == OFF_)                                                 \
-    return launch_f32_any<S_, T_, OFF_>(bf, exact, planes, in, in_h, in_w, in_row_stride,        \
+    return launch_f32_any<S_, T_, OFF_>(ep != nullptr, bf, exact, planes, in, in_h, in_w, in_row_stride,        \
                                         in_plane_stride, row_base, row_weights, out_h, col_base, \
                                         col_weights, out_w, out, out_row_stride,                 \
                                         out_plane_stride, ek, st);
