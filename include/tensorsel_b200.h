@@ -13,6 +13,11 @@
  *   - Device pointers are caller-owned (torch tensors / cudaMalloc); all
  *     kernels are enqueued on the caller's stream (a cudaStream_t passed as
  *     void*, NULL = legacy default stream) and never synchronise it.
+ *   - Images are planar with row / plane strides in elements that are
+ *     multiples of 16 bytes (TMA).  Output rows are written in whole 16-byte
+ *     units: the bytes from the last column to the next 16-byte boundary of
+ *     a row may be overwritten (they belong to the row's stride); nothing
+ *     beyond them is touched (tests/test_gpu_guards.py).
  *   - Status codes map 1:1 onto the reference exception classes:
  *       TS_ERR_OUT_OF_BOUNDS      -> interp.OutOfBounds / layout.OutOfBounds
  *       TS_ERR_PHASE_MISMATCH     -> layout.PhaseMismatch        (layout.py:24)

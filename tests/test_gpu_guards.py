@@ -5,6 +5,10 @@ Each kernel writes its output through the C ABI into a view of a larger
 buffer: canary bands before and after the output, and padding columns
 between rows (row stride > width).  The canaries must survive bit for bit,
 and the strided output must equal a compact call of the same pipeline.
+The ABI's row contract (include/tensorsel_b200.h): a row is written in
+whole 16-byte units — TMA stores fill the last partial 16 bytes of a row —
+so the bytes up to the next 16-byte boundary belong to the row (row strides
+are multiples of 16 bytes); everything past that must stay untouched.
 Inputs sit between NaN guard bands; a read outside the image would turn
 outputs into NaN.  Ragged sizes exercise the edge tiles of every kernel.
 """
@@ -54,7 +58,8 @@ def _canaries_intact(buf, out, W):
     o0 = out.data_ptr() - buf.data_ptr()
     o0 //= buf.element_size()
     P, H, rs = out.shape
-    idx = torch.arange(P * H * rs, device=buf.device).view(P, H, rs)[:, :, :W].reshape(-1) + o0
+    W16 = -(-W * buf.element_size() // 16) * 16 // buf.element_size()  # the row's 16-byte units
+    idx = torch.arange(P * H * rs, device=buf.device).view(P, H, rs)[:, :, :W16].reshape(-1) + o0
     inner[idx] = True
     return bool(((bits == want) | inner).all())
 
