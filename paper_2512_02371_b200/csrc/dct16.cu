@@ -255,6 +255,17 @@ __device__ __forceinline__ Region region_of(const Params& P, int t) {
   return r;
 }
 
+// The persistent loop's next region (t += gridDim.x) by mixed-radix
+// addition of the precomputed grid stride: no runtime division per band.
+__device__ __forceinline__ Region region_next(const Params& P, Region r, const Region& step) {
+  r.rx += step.rx;
+  if (r.rx >= P.nrx) r.rx -= P.nrx, ++r.ry;
+  r.ry += step.ry;
+  if (r.ry >= P.nry) r.ry -= P.nry, ++r.p;
+  r.p += step.p;
+  return r;
+}
+
 template <int BW, typename OutT, bool SOFT, bool EPI = false>
 __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     dct16_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
@@ -319,9 +330,10 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       bulk_g2s(base + kOffC, P.consts, kConstBytes, cbar);
     }
     int it = 0;
-    for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
+    const Region step = region_of(P, gridDim.x);
+    Region R = region_of(P, blockIdx.x);
+    for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it, R = region_next(P, R, step)) {
       const int s = it & 1;
-      const Region R = region_of(P, t);
       const int Y = R.ry * kOutRows, X = R.rx * kOut;
       uint8_t* dst = base + kOffX + s * kBandBytes;
       if (lane == 0) {
@@ -504,8 +516,9 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     int pX = 0, pY = 0, pP = 0, pit = -1;  // band whose E4 is pending
     int it = 0;
     uint32_t ph = 0;
-    for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it) {
-      const Region R = region_of(P, t);
+    const Region step = region_of(P, gridDim.x);
+    Region R = region_of(P, blockIdx.x);
+    for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it, R = region_next(P, R, step)) {
       const int Y = R.ry * kOutRows, X = R.rx * kOut;
       for (int p = 0; p < 2; ++p) {
         // ---- C1: D1 (f32, lane f, BW columns) -> bf16 pairs: hi at [0, BW/2), lo at [BW/2, BW)
