@@ -77,8 +77,13 @@ constexpr uint32_t kCS7 = 3 * kStripBytes;  // S1 strip: hi, mid, lo
 constexpr uint32_t kCB3 = kCS7 + 7936;
 constexpr uint32_t kCB5 = kCB3 + 1024;
 constexpr uint32_t kConstBytes = kCB5 + 1024;
-constexpr int kBandRows = 128;  // band rows (input), 112 output rows
-constexpr int kOutRows = 112;
+// A CTA walks a column strip (BW input columns -> BW - 16 output columns)
+// from the top of the image to the bottom in groups of 8 tile rows: group g
+// reads input rows 64g - 8 .. 64g + 72 (80 rows; the last 8 only meet zero
+// weights) and completes output rows 64g - 8 .. 64g + 56.
+constexpr int kGroupRows = 80;  // staged input rows per group
+constexpr int kGroupOut = 64;   // output rows completed per group
+constexpr int kNX = 3;          // input group buffers
 
 constexpr uint32_t round1k(uint32_t v) { return (v + 1023u) / 1024u * 1024u; }
 
@@ -93,12 +98,12 @@ struct Geo {
   static constexpr int kThreads = 64 + kEpiThreads;  // + loader warp, MMA warp
   static constexpr int kNq0 = BW / 16, kNq1 = BW / 16 - 1;  // tiles per column phase
   static constexpr int kChunks = kNq0 + kNq1;                // 16-column chunks of D2
-  static constexpr uint32_t kBandBytes = kBandRows * BW * 2;  // BW/64 SW128 boxes
-  static constexpr uint32_t kOffX = 0;                        // 2 band buffers
-  static constexpr uint32_t kB7Bytes = kBandRows * BW * 2;    // S7 B operand (fp16)
-  static constexpr uint32_t kOffB7 = 2 * kBandBytes;
-  static constexpr uint32_t kOffOut = kOffB7 + kB7Bytes;      // staging (f32 worst case)
-  static constexpr uint32_t kOffC = kOffOut + round1k(kOutRows * kOutW * 4);
+  static constexpr uint32_t kBufBytes = kGroupRows * BW * 2;  // BW/64 SW128 boxes
+  static constexpr uint32_t kOffX = 0;                        // kNX group buffers
+  static constexpr uint32_t kB7Bytes = 128 * BW * 2;          // S7 B operand (fp16), x2
+  static constexpr uint32_t kOffB7 = kNX * kBufBytes;
+  static constexpr uint32_t kOffOut = kOffB7 + 2 * kB7Bytes;  // staging (f32 worst case)
+  static constexpr uint32_t kOffC = kOffOut + round1k(kGroupOut * kOutW * 4);
   static constexpr uint32_t kOffBar = kOffC + kConstBytes;
   static constexpr uint32_t kSmem = kOffBar + 256 + 1024;
   // TMEM columns: D1 f32 / packed pairs (hi [0, BW/2), lo [BW/2, BW));
@@ -114,7 +119,9 @@ struct Geo {
 };
 
 struct Params {
-  int planes, H, W, nry, nrx, nregions;
+  int planes, H, W;
+  int nstrips, ngroups, nunits;  // strips per plane, groups per strip, units
+  int nseg, seg_groups;          // segments per strip and groups per segment
   float threshold;
   int soft;                 // 0 hard, 1 soft coring
   const uint8_t* consts;    // kConstBytes
@@ -186,10 +193,12 @@ __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// Byte offset of element (row, col) in a 128-row x 128-col bf16 operand made
-// of two 64-column 128B-swizzled halves (the TMA band layout, and B7).
+// Byte offset of element (row, col) in a ROWS-row bf16/fp16 operand made of
+// 64-column 128B-swizzled halves (the TMA group layout, and B7).
+template <int ROWS>
 __device__ __forceinline__ uint32_t sw_off(int row, int col) {
-  return (col >> 6) * 16384u + row * 128u + ((((col & 63) >> 3) ^ (row & 7)) << 4) + (col & 7) * 2u;
+  return (col >> 6) * (ROWS * 128u) + row * 128u + ((((col & 63) >> 3) ^ (row & 7)) << 4) +
+         (col & 7) * 2u;
 }
 
 // fp16 hi/lo split of a pair: hi = RNE(a), lo = RNE(a - hi).  |a - hi - lo|
@@ -207,16 +216,17 @@ __device__ __forceinline__ uint32_t hi_lo(float a, float b, uint32_t* lo) {
 template <int BW>
 __device__ __forceinline__ void fix_edges(uint8_t* bx, int Y, int X, int H, int W, int lane) {
   constexpr int kChunkCols = BW / 8;  // 16-byte chunks per band row
+  constexpr uint32_t kHalf = kGroupRows * 128u;  // bytes per 64-column half
   int r0[2], rs[2], nr = 0;
   if (Y == 0) { r0[nr] = 0; rs[nr] = 8; ++nr; }
-  if (H - Y + 8 < kBandRows) { r0[nr] = H - Y + 8; rs[nr] = H - Y + 7; ++nr; }
+  if (H - Y + 8 < kGroupRows) { r0[nr] = H - Y + 8; rs[nr] = H - Y + 7; ++nr; }
   for (int e = 0; e < nr; ++e) {
-    const int rows = min(8, kBandRows - r0[e]);
+    const int rows = min(8, kGroupRows - r0[e]);
     for (int idx = lane; idx < rows * kChunkCols; idx += 32) {
       const int br = r0[e] + idx / kChunkCols, j = idx % kChunkCols, h = j >> 3, cc = j & 7;
-      const uint4 v = *reinterpret_cast<const uint4*>(bx + h * 16384 + rs[e] * 128 +
+      const uint4 v = *reinterpret_cast<const uint4*>(bx + h * kHalf + rs[e] * 128 +
                                                       ((cc ^ (rs[e] & 7)) << 4));
-      *reinterpret_cast<uint4*>(bx + h * 16384 + br * 128 + ((cc ^ (br & 7)) << 4)) = v;
+      *reinterpret_cast<uint4*>(bx + h * kHalf + br * 128 + ((cc ^ (br & 7)) << 4)) = v;
     }
   }
   __syncwarp();
@@ -224,10 +234,10 @@ __device__ __forceinline__ void fix_edges(uint8_t* bx, int Y, int X, int H, int 
   if (X == 0) { c0[nc] = 0; cs[nc] = 8; ++nc; }
   if (W - X + 8 < BW) { c0[nc] = W - X + 8; cs[nc] = W - X + 7; ++nc; }
   for (int e = 0; e < nc; ++e) {
-    for (int br = lane; br < kBandRows; br += 32) {
-      const uint32_t v = *reinterpret_cast<const uint16_t*>(bx + sw_off(br, cs[e]));
+    for (int br = lane; br < kGroupRows; br += 32) {
+      const uint32_t v = *reinterpret_cast<const uint16_t*>(bx + sw_off<kGroupRows>(br, cs[e]));
       const uint32_t w = v | (v << 16);
-      *reinterpret_cast<uint4*>(bx + sw_off(br, c0[e])) = make_uint4(w, w, w, w);
+      *reinterpret_cast<uint4*>(bx + sw_off<kGroupRows>(br, c0[e])) = make_uint4(w, w, w, w);
     }
   }
   fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05 operand reads
@@ -242,28 +252,57 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar, int lane) {
   if (lane == 0) mbar_arrive(bar);
 }
 
-struct Region {
-  int p, ry, rx;
+// Work unit: one vertical segment of one column strip of one plane (a strip
+// is split into P.nseg segments only when there are too few strips to fill
+// the GPU).  A segment after the first starts with a warm-up group — the
+// group above it, computed but not stored — whose last tile row completes
+// the segment's first 8 output rows.
+struct Unit {
+  int seg, sx, p;
 };
 
-__device__ __forceinline__ Region region_of(const Params& P, int t) {
-  Region r;
-  r.rx = t % P.nrx;
-  const int rest = t / P.nrx;
-  r.ry = rest % P.nry;
-  r.p = rest / P.nry;
-  return r;
+__device__ __forceinline__ Unit unit_of(const Params& P, int t) {
+  Unit u;
+  u.seg = t % P.nseg;
+  const int rest = t / P.nseg;
+  u.sx = rest % P.nstrips;
+  u.p = rest / P.nstrips;
+  return u;
 }
 
-// The persistent loop's next region (t += gridDim.x) by mixed-radix
-// addition of the precomputed grid stride: no runtime division per band.
-__device__ __forceinline__ Region region_next(const Params& P, Region r, const Region& step) {
-  r.rx += step.rx;
-  if (r.rx >= P.nrx) r.rx -= P.nrx, ++r.ry;
-  r.ry += step.ry;
-  if (r.ry >= P.nry) r.ry -= P.nry, ++r.p;
-  r.p += step.p;
-  return r;
+// The persistent loop's next unit (u += gridDim.x) by mixed-radix addition
+// of the precomputed grid stride: no runtime division per unit.
+__device__ __forceinline__ Unit unit_add(const Params& P, Unit u, const Unit& step) {
+  u.seg += step.seg;
+  if (u.seg >= P.nseg) u.seg -= P.nseg, ++u.sx;
+  u.sx += step.sx;
+  if (u.sx >= P.nstrips) u.sx -= P.nstrips, ++u.p;
+  u.p += step.p;
+  return u;
+}
+
+// Position in this CTA's stream of groups: unit, group row g, the unit's
+// first and end group.
+struct GroupIt {
+  Unit u;
+  int g, g0, g1;
+  __device__ __forceinline__ bool valid(const Params& P) const { return u.p < P.planes; }
+  __device__ __forceinline__ bool warm() const { return u.seg > 0 && g == g0; }
+  __device__ __forceinline__ bool first() const { return g == g0; }
+};
+
+__device__ __forceinline__ GroupIt unit_start(const Params& P, const Unit& u) {
+  GroupIt it;
+  it.u = u;
+  it.g0 = u.seg * P.seg_groups - (u.seg > 0 ? 1 : 0);
+  it.g1 = min((u.seg + 1) * P.seg_groups, P.ngroups);
+  it.g = it.g0;
+  return it;
+}
+
+__device__ __forceinline__ GroupIt group_next(const Params& P, GroupIt it, const Unit& step) {
+  if (++it.g < it.g1) return it;
+  return unit_start(P, unit_add(P, it.u, step));
 }
 
 template <int BW, typename OutT, bool SOFT, bool EPI = false>
@@ -272,7 +311,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
                  const __grid_constant__ Params P) {
   using G = Geo<BW>;
   constexpr int kEpiThreads = G::kEpiThreads;
-  constexpr uint32_t kBandBytes = G::kBandBytes, kOffX = G::kOffX, kOffB7 = G::kOffB7;
+  constexpr uint32_t kBufBytes = G::kBufBytes, kOffX = G::kOffX, kOffB7 = G::kOffB7;
   constexpr uint32_t kOffOut = G::kOffOut, kOffC = G::kOffC;
   constexpr uint32_t kTD1 = G::kTD1, kTD2 = G::kTD2, kTD3 = G::kTD3, kTD4 = G::kTD4;
   constexpr int kOut = G::kOutW;
@@ -281,23 +320,23 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_s - raw_s);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + G::kOffBar);
-  uint64_t* xfull = bars;        // [2]
-  uint64_t* xempty = bars + 2;   // [2]
-  uint64_t* xready = bars + 4;   // [2]
-  uint64_t* s1done = bars + 6;
-  uint64_t* c1 = bars + 7;
-  uint64_t* s3done = bars + 8;   // [2]: column phase q = 0 / 1 tiles done
-  uint64_t* e2 = bars + 10;      // [2]: their coefficients cored
-  uint64_t* s5done = bars + 12;
-  uint64_t* e3 = bars + 13;
-  uint64_t* s7done = bars + 14;
-  uint64_t* e4 = bars + 15;
-  uint64_t* cbar = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* xfull = bars;              // [kNX]
+  uint64_t* xempty = bars + kNX;       // [kNX]
+  uint64_t* xready = bars + 2 * kNX;   // [kNX]
+  uint64_t* s1done = bars + 3 * kNX;
+  uint64_t* c1 = s1done + 1;
+  uint64_t* s3done = s1done + 2;       // [2]: column phase q = 0 / 1 tiles done
+  uint64_t* e2 = s1done + 4;           // [2]: their coefficients cored
+  uint64_t* s5done = s1done + 6;
+  uint64_t* e3 = s1done + 7;
+  uint64_t* s7done = s1done + 8;
+  uint64_t* e4 = s1done + 9;
+  uint64_t* cbar = s1done + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s1done + 11);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kNX; ++s) {
       mbar_init(&xfull[s], 1);
       mbar_init(&xempty[s], 1);
       mbar_init(&xready[s], 1);
@@ -308,10 +347,10 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     mbar_init(s5done, 1);
     mbar_init(s7done, 1);
     mbar_init(c1, kEpiThreads / 32);  // one arrival per epilogue warp
-    mbar_init(&e2[0], kEpiThreads / 32);  // one arrival per epilogue warp
-    mbar_init(&e2[1], kEpiThreads / 32);  // one arrival per epilogue warp
-    mbar_init(e3, kEpiThreads / 32);  // one arrival per epilogue warp
-    mbar_init(e4, kEpiThreads / 32);  // one arrival per epilogue warp
+    mbar_init(&e2[0], kEpiThreads / 32);
+    mbar_init(&e2[1], kEpiThreads / 32);
+    mbar_init(e3, kEpiThreads / 32);
+    mbar_init(e4, kEpiThreads / 32);
     mbar_init(cbar, 1);
     fence_barrier_init();
     prefetch_tmap(&tm_in);
@@ -322,6 +361,10 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // this CTA's groups: units u = blockIdx.x, += gridDim.x, each walked top
+  // to bottom in groups of 8 tile rows
+  const Unit ustep = unit_of(P, gridDim.x);
+  const GroupIt it0 = unit_start(P, unit_of(P, blockIdx.x));
 
   if (warp == 0) {
     // ------------------------------------------------------------ loader + edge fix-up
@@ -329,24 +372,23 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       mbar_arrive_expect_tx(cbar, kConstBytes);
       bulk_g2s(base + kOffC, P.consts, kConstBytes, cbar);
     }
-    int it = 0;
-    const Region step = region_of(P, gridDim.x);
-    Region R = region_of(P, blockIdx.x);
-    for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it, R = region_next(P, R, step)) {
-      const int s = it & 1;
-      const int Y = R.ry * kOutRows, X = R.rx * kOut;
-      uint8_t* dst = base + kOffX + s * kBandBytes;
+    int i = 0;
+    for (GroupIt gi = it0; gi.valid(P); gi = group_next(P, gi, ustep), ++i) {
+      const int s = i % kNX;
+      const int Y = kGroupOut * gi.g, X = gi.u.sx * kOut;
+      const Unit& U = gi.u;
+      uint8_t* dst = base + kOffX + s * kBufBytes;
       if (lane == 0) {
-        mbar_wait(&xempty[s], ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&xfull[s], kBandBytes);
+        mbar_wait(&xempty[s], ((i / kNX) & 1) ^ 1);
+        mbar_arrive_expect_tx(&xfull[s], kBufBytes);
 #pragma unroll
         for (int h = 0; h < BW / 64; ++h)
-          tma_load_3d(dst + h * kBandRows * 128, &tm_in, &xfull[s], X - 8 + 64 * h, Y - 8, R.p);
+          tma_load_3d(dst + h * kGroupRows * 128, &tm_in, &xfull[s], X - 8 + 64 * h, Y - 8, U.p);
       }
       __syncwarp();
-      const bool edge = Y == 0 || X == 0 || P.H - Y + 8 < kBandRows || P.W - X + 8 < BW;
+      const bool edge = Y == 0 || X == 0 || P.H - Y + 8 < kGroupRows || P.W - X + 8 < BW;
       if (edge) {
-        mbar_wait(&xfull[s], (it >> 1) & 1);
+        mbar_wait(&xfull[s], (i / kNX) & 1);
         fix_edges<BW>(dst, Y, X, P.H, P.W, lane);
       }
       if (lane == 0) mbar_arrive(&xready[s]);
@@ -360,92 +402,94 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     const uint32_t c4 = (base_s + kOffC) >> 4;
     const uint64_t b3 = make_sdesc(base_s + kOffC + kCB3, 128u, 256u, kSwizzleNone);
     const uint64_t b5 = make_sdesc(base_s + kOffC + kCB5, 128u, 256u, kSwizzleNone);
-    const uint64_t b7 = make_sdesc(base_s + kOffB7, 16384u, 1024u, kSwizzle128B);
+    const uint64_t b7d[2] = {make_sdesc(base_s + kOffB7, 16384u, 1024u, kSwizzle128B),
+                             make_sdesc(base_s + kOffB7 + G::kB7Bytes, 16384u, 1024u, kSwizzle128B)};
     mbar_wait(cbar, 0);
-    // S1: D1 = T_g · X for tile group g (tiles t = 8g .. 8g + 7, starting at
-    // band row 8t; lane 16 (t - 8g) + k).  K-step m (band rows 16m ..) feeds
-    // tiles 2m - 1, 2m, 2m + 1, so group 0 needs K-steps 0..4 and group 1
-    // K-steps 4..7: 9 K-steps x (hi, lo) per band.  A = a window of one
+    // S1: D1 = T · X for the group's 8 tile rows (tile k starts at group
+    // buffer row 8k; lane 16k + freq).  K-step m (buffer rows 16m ..) feeds
+    // tiles 2m - 1, 2m, 2m + 1: 5 K-steps x (hi, mid, lo) of a window of one
     // constant strip, moved 32 lanes per K-step.
-    auto issue_s1 = [&](int s, int g) {
-      const uint64_t bx = make_sdesc(base_s + kOffX + s * kBandBytes, 16384u, 1024u, kSwizzle128B);
+    auto issue_s1 = [&](int s) {
+      const uint64_t bx =
+          make_sdesc(base_s + kOffX + s * kBufBytes, kGroupRows * 128u, 1024u, kSwizzle128B);
       tc_fence_after();
 #pragma unroll
-      for (int m = 4 * g; m < 5 + 3 * g; ++m) {
-        const uint32_t so = 256u - 64u * m + 256u * g;  // strip window, 16-byte units
-        const uint32_t acc = m > 4 * g ? 1u : 0u;
+      for (int m = 0; m < 5; ++m) {
+        const uint32_t so = 256u - 64u * m;  // strip window, 16-byte units
+        const uint32_t acc = m > 0 ? 1u : 0u;
         mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + so), bx + 128u * m, id128, acc);  // hi
         mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + kStripBytes / 16 + so), bx + 128u * m, id128,
                          1u);
         mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + 2 * kStripBytes / 16 + so), bx + 128u * m,
                          id128, 1u);
       }
-      mma_commit_elect(s1done);  // before any later S7: C1 must not wait for it
-      if (g == 1) mma_commit_elect(&xempty[s]);
+      mma_commit_elect(s1done);
+      mma_commit_elect(&xempty[s]);
     };
-    int it = 0;
-    uint32_t ph = 0;  // phase of the per-row-phase barriers (two completions per band)
-    int t = blockIdx.x;
-    if (t < P.nregions) {
+    if (it0.valid(P)) {
       mbar_wait(&xfull[0], 0);
       mbar_wait(&xready[0], 0);
-      if (lane == 0) stamp(P, 0, 7);
-      issue_s1(0, 0);
+      issue_s1(0);
     }
-    for (; t < P.nregions; t += gridDim.x, ++it) {
-      const int s = it & 1;
-      for (int p = 0; p < 2; ++p) {
-        // ---- S3: row forward, A = packed D1 from TMEM
-        mbar_wait(c1, ph);
-        tc_fence_after();
+    int i = 0;
+    for (GroupIt gi = it0; gi.valid(P); ++i) {
+      const uint32_t ph = i & 1;
+      const GroupIt nx = group_next(P, gi, ustep);
+      // ---- S3: row forward, A = packed D1 from TMEM
+      mbar_wait(c1, ph);
+      tc_fence_after();
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+      for (int q = 0; q < 2; ++q) {
 #pragma unroll
-          for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j) {
-            const uint32_t pc = 8u * j + 4u * q;  // packed column of the tile's first sample
-            const uint32_t d = tmem + kTD2 + 16u * (G::kNq0 * q + j);
-            mma_f16_ts_elect(d, tmem + kTD1 + pc, b3, id16h, 0u);
-            mma_f16_ts_elect(d, tmem + kTD1 + BW / 2 + pc, b3, id16h, 1u);
-            mma_f16_ts_elect(d, tmem + kTD1 + pc, b3 + 32u, id16h, 1u);
-          }
-          mma_commit_elect(&s3done[q]);  // E2 cores column phase q while S3 runs q + 1
+        for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j) {
+          const uint32_t pc = 8u * j + 4u * q;  // packed column of the tile's first sample
+          const uint32_t d = tmem + kTD2 + 16u * (G::kNq0 * q + j);
+          mma_f16_ts_elect(d, tmem + kTD1 + pc, b3, id16h, 0u);
+          mma_f16_ts_elect(d, tmem + kTD1 + BW / 2 + pc, b3, id16h, 1u);
+          mma_f16_ts_elect(d, tmem + kTD1 + pc, b3 + 32u, id16h, 1u);
         }
-        // The next row phase's S1 (this band's p = 1, or the next band's p = 0)
-        // goes right behind S3: D1 is free once S3 has read it (in-order
-        // tensor pipe), so its C1 can follow this phase's E3 without a wait.
-        if (p == 0) {
-          issue_s1(s, 1);
-        } else if (t + static_cast<int>(gridDim.x) < P.nregions) {
-          const int s2 = (it + 1) & 1;
-          mbar_wait(&xfull[s2], ((it + 1) >> 1) & 1);
-          mbar_wait(&xready[s2], ((it + 1) >> 1) & 1);
-          if (lane == 0) stamp(P, it + 1, 7);
-          issue_s1(s2, 0);
-        }
-        // ---- S5: row inverse (TS f16, A = cored D2 packed at kTD2 + 8 ch) into
-        // D3, which overlays the q = 1 f32 chunks: after all of E2
-        mbar_wait(&e2[1], ph);
-        tc_fence_after();
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-#pragma unroll
-          for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j)
-            mma_f16_ts_elect(tmem + kTD3 + 16u * j + 8u * q, tmem + kTD2 + 8u * (G::kNq0 * q + j),
-                             b5, id16h, q > 0 ? 1u : 0u);
-        }
-        mma_commit_elect(s5done);
-        mbar_wait(e3, ph);
-        // ---- S7: column inverse, D4 += T_pᵀ · B7 (fp16)
-        if (p == 0 && it > 0) mbar_wait(e4, (it - 1) & 1);  // previous band's E4 read D4
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < (p == 0 ? 8 : 7); ++k) {  // tile t = 8p + k
-          const uint64_t ad = a_tmpl | (c4 + kCS7 / 16 + (15u - 8u * p - k) * 16u);
-          mma_f16_ss_elect(tmem + kTD4, ad, b7 + 128u * k, id128h, (p > 0 || k > 0) ? 1u : 0u);
-        }
-        mma_commit_elect(s7done);
-        ph ^= 1;
+        mma_commit_elect(&s3done[q]);  // E2 cores column phase q while S3 runs q + 1
       }
+      // The next group's S1 goes right behind S3: D1 is free once S3 has
+      // read it (in-order tensor pipe), so its C1 can follow this group's E3.
+      if (nx.valid(P)) {
+        const int s2 = (i + 1) % kNX;
+        mbar_wait(&xfull[s2], ((i + 1) / kNX) & 1);
+        mbar_wait(&xready[s2], ((i + 1) / kNX) & 1);
+        issue_s1(s2);
+      }
+      // ---- S5: row inverse (TS f16, A = cored D2 packed at kTD2 + 8 ch) into
+      // D3, which overlays the q = 1 f32 chunks: after all of E2
+      mbar_wait(&e2[1], ph);
+      tc_fence_after();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+#pragma unroll
+        for (int j = 0; j < (q == 0 ? G::kNq0 : G::kNq1); ++j)
+          mma_f16_ts_elect(tmem + kTD3 + 16u * j + 8u * q, tmem + kTD2 + 8u * (G::kNq0 * q + j),
+                           b5, id16h, q > 0 ? 1u : 0u);
+      }
+      mma_commit_elect(s5done);
+      mbar_wait(e3, ph);
+      // ---- S7: column inverse, D4 = Σ_k T_kᵀ · B7_k (fp16); D4 lane r =
+      // input row 64g - 16 + r.  Tile k (k = -1 .. 7, -1 = the previous
+      // group's last tile, still in the other B7 buffer) covers lanes
+      // 8k + 8 .. 8k + 24, so lanes 8 .. 71 (rows 64g - 8 .. 64g + 56) are
+      // complete: no row halo is recomputed between groups.
+      if (i > 0) mbar_wait(e4, (i - 1) & 1);  // the previous group's E4 has read D4
+      tc_fence_after();
+      const bool prev = !gi.first();  // the group above is this unit's, in the other B7
+      if (prev)
+        mma_f16_ss_elect(tmem + kTD4, a_tmpl | (c4 + kCS7 / 16 + 15u * 16u),
+                         b7d[(i - 1) & 1] + 128u * 7, id128h, 0u);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t ad = a_tmpl | (c4 + kCS7 / 16 + (14u - k) * 16u);
+        mma_f16_ss_elect(tmem + kTD4, ad, b7d[i & 1] + 128u * k, id128h,
+                         (prev || k > 0) ? 1u : 0u);
+      }
+      mma_commit_elect(s7done);
+      gi = nx;
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..)
@@ -458,45 +502,44 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t tl = tmem + lane_off;
     const int et = threadIdx.x - 64;
-    auto do_e4 = [&](int it4, int X4, int Y4, int p4) {
-        // ---- E4: D4 (lane = band row r, columns = band column c) -> output block
-        // (S7 completes twice per band; E4 waits the second: parity 1)
-        mbar_wait(s7done, 1u);
+    auto do_e4 = [&](int i4, int X4, int Y4, int p4, bool store) {
+        // ---- E4: D4 lanes 8 .. 71 (rows Y4 - 8 .. Y4 + 56) -> output block
+        mbar_wait(s7done, i4 & 1);
         tc_fence_after();
-        if (et == 0) stamp(P, it4, 22);
-        if (sp == 0) dbg_dump(P, it4, 3, 0, tl + kTD4, row, BW);
         if (et == 0) bulk_wait_read0();
         named_bar_sync(1, kEpiThreads);
-        {
-          uint32_t v[2][16];
+        uint32_t v[2][16];
+        if (quarter < 3) {  // lanes 0 .. 95 (lanes >= 72 belong to no complete row)
           tmem_ld16(tl + kTD4 + 32u * sp, v[0]);
           tmem_ld16(tl + kTD4 + 32u * sp + 16u, v[1]);
           tmem_wait_ld();
-          tc_fence_before();
-          warp_arrive(e4, lane);
-          if (row >= 8 && row < 8 + kOutRows) {
+        }
+        tc_fence_before();
+        warp_arrive(e4, lane);  // D4 is free for the next group's S7
+        if (store) {
+          if (row >= 8 && row < 8 + kGroupOut) {
             uint8_t* orow = base + kOffOut + (row - 8) * kOut * sizeof(OutT);
             // band columns 8..BW-9 -> output columns 0..kOut-1, 8 at a time
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const int c = 32 * sp + 8 * g;
+            for (int g8 = 0; g8 < 4; ++g8) {
+              const int c = 32 * sp + 8 * g8;
               if (c >= 8 && c < 8 + kOut) {
-                const uint32_t* src = &v[g >> 1][8 * (g & 1)];
+                const uint32_t* src = &v[g8 >> 1][8 * (g8 & 1)];
                 if constexpr (sizeof(OutT) == 2) {
                   uint32_t pk[4];
 #pragma unroll
-                  for (int i = 0; i < 4; ++i)
-                    pk[i] = EPI ? epi_bf16x2(P.ep, __uint_as_float(src[2 * i]),
-                                             __uint_as_float(src[2 * i + 1]))
-                                : pack_bf16x2(__uint_as_float(src[2 * i]),
-                                              __uint_as_float(src[2 * i + 1]));
+                  for (int e = 0; e < 4; ++e)
+                    pk[e] = EPI ? epi_bf16x2(P.ep, __uint_as_float(src[2 * e]),
+                                             __uint_as_float(src[2 * e + 1]))
+                                : pack_bf16x2(__uint_as_float(src[2 * e]),
+                                              __uint_as_float(src[2 * e + 1]));
                   *reinterpret_cast<uint4*>(orow + (c - 8) * 2) =
                       make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 } else {
                   uint32_t f[8];
 #pragma unroll
-                  for (int i = 0; i < 8; ++i)
-                    f[i] = EPI ? __float_as_uint(epi_f32(P.ep, __uint_as_float(src[i]))) : src[i];
+                  for (int e = 0; e < 8; ++e)
+                    f[e] = EPI ? __float_as_uint(epi_f32(P.ep, __uint_as_float(src[e]))) : src[e];
                   *reinterpret_cast<uint4*>(orow + (c - 8) * 4) = make_uint4(f[0], f[1], f[2], f[3]);
                   *reinterpret_cast<uint4*>(orow + (c - 8) * 4 + 16) =
                       make_uint4(f[4], f[5], f[6], f[7]);
@@ -505,135 +548,119 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
             }
           }
         }
+        if (!store) return;  // a warm-up group: computed for its last tile row only
         fence_proxy_async_smem();
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
-          tma_store_3d(&tm_out, base + kOffOut, X4, Y4, p4);
+          tma_store_3d(&tm_out, base + kOffOut, X4, Y4 - 8, p4);
           bulk_commit();
-          stamp(P, it4, 23);
         }
     };
-    int pX = 0, pY = 0, pP = 0, pit = -1;  // band whose E4 is pending
-    int it = 0;
-    uint32_t ph = 0;
-    const Region step = region_of(P, gridDim.x);
-    Region R = region_of(P, blockIdx.x);
-    for (int t = blockIdx.x; t < P.nregions; t += gridDim.x, ++it, R = region_next(P, R, step)) {
-      const int Y = R.ry * kOutRows, X = R.rx * kOut;
-      for (int p = 0; p < 2; ++p) {
-        // ---- C1: D1 (f32, lane f, BW columns) -> bf16 pairs: hi at [0, BW/2), lo at [BW/2, BW)
-        mbar_wait(s1done, ph);
-        tc_fence_after();
-        if (et == 0) stamp(P, it, 12 * p + 0);
-        if (sp == 0) dbg_dump(P, it, 0, p, tl + kTD1, row, BW);
-        {
-          uint32_t v[2][16];
-          tmem_ld16(tl + kTD1 + 32u * sp, v[0]);
-          tmem_ld16(tl + kTD1 + 32u * sp + 16u, v[1]);
-          tmem_wait_ld();
-          named_bar_sync(1, kEpiThreads);  // every split has read its f32 columns
-          uint32_t hi[16], lo[16];
+    int pX = 0, pY = 0, pP = 0, pi = -1;  // group whose E4 is pending
+    bool pstore = false;
+    int i = 0;
+    for (GroupIt gi = it0; gi.valid(P); gi = group_next(P, gi, ustep), ++i) {
+      const uint32_t ph = i & 1;
+      const int Y = kGroupOut * gi.g, X = gi.u.sx * kOut;
+      // ---- C1: D1 (f32, lane f, BW columns) -> fp16 hi/lo pairs: hi at [0, BW/2), lo at [BW/2, BW)
+      mbar_wait(s1done, ph);
+      tc_fence_after();
+      {
+        uint32_t v[2][16];
+        tmem_ld16(tl + kTD1 + 32u * sp, v[0]);
+        tmem_ld16(tl + kTD1 + 32u * sp + 16u, v[1]);
+        tmem_wait_ld();
+        named_bar_sync(1, kEpiThreads);  // every split has read its f32 columns
+        uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            hi[e] = hi_lo(__uint_as_float(v[e >> 3][(2 * e) & 15]),
-                          __uint_as_float(v[e >> 3][((2 * e) & 15) + 1]), &lo[e]);
-          tmem_st16(tl + kTD1 + 16u * sp, hi);
-          tmem_st16(tl + kTD1 + BW / 2 + 16u * sp, lo);
+        for (int e = 0; e < 16; ++e)
+          hi[e] = hi_lo(__uint_as_float(v[e >> 3][(2 * e) & 15]),
+                        __uint_as_float(v[e >> 3][((2 * e) & 15) + 1]), &lo[e]);
+        tmem_st16(tl + kTD1 + 16u * sp, hi);
+        tmem_st16(tl + kTD1 + BW / 2 + 16u * sp, lo);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      warp_arrive(c1, lane);
+      if (pi >= 0) {  // the previous group's E4, off the critical path
+        do_e4(pi, pX, pY, pP, pstore);
+        pi = -1;
+      }
+      // ---- E2: coring of D2 (lane f, columns 16*(kNq0*q+j) + l) in place,
+      // one column phase at a time
+      const bool dc_row = (row & 15) == 0;
+      const float thr = P.threshold, nthr_big = -thr * 0x1p100f;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        mbar_wait(&s3done[q], ph);
+        tc_fence_after();
+        const int ch0 = q == 0 ? 0 : G::kNq0, ch1 = q == 0 ? G::kNq0 : G::kChunks;
+        uint32_t v[2][16];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          if (ch0 + sp + G::kSplits * c < ch1)
+            tmem_ld16(tl + kTD2 + 16u * (ch0 + sp + G::kSplits * c), v[c]);
+        tmem_wait_ld();
+        // the packed q = 0 pairs overwrite f32 chunks other warps still read
+        if (q == 0) named_bar_sync(1, kEpiThreads);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int ch = ch0 + sp + G::kSplits * c;
+          if (ch < ch1) {
+            const uint32_t dc = v[c][0];
+#pragma unroll
+            for (int l = 0; l < 16; ++l) {
+              const float x = __uint_as_float(v[c][l]);
+              float y;
+              // coring on the FMA pipe (the ALU pipe, 64 lanes/clk, also
+              // runs the fp16 packing): keep = sat((|x| - thr) * 2^100) is 1
+              // for |x| > thr and 0 below it
+              if constexpr (SOFT) {
+                const float d = fabsf(x) - thr;
+                y = copysignf(d * __saturatef(d * 0x1p100f), x);
+              } else {
+                y = x * __saturatef(fmaf(fabsf(x), 0x1p100f, nthr_big));
+              }
+              v[c][l] = __float_as_uint(y);
+            }
+            if (dc_row) v[c][0] = dc;  // DC coefficient kept
+            uint32_t h[8];  // fp16 pairs: the S5 A operand (K = 16 in 8 columns)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              h[e] = pack_f16x2(__uint_as_float(v[c][2 * e]), __uint_as_float(v[c][2 * e + 1]));
+            tmem_st8(tl + kTD2 + 8u * ch, h);
+          }
         }
         tmem_wait_st();
         tc_fence_before();
-        warp_arrive(c1, lane);
-        if (et == 0) stamp(P, it, 12 * p + 1);
-        if (p == 0 && pit >= 0) {
-          do_e4(pit, pX, pY, pP);
-          pit = -1;
-        }
-        // ---- E2: coring of D2 (lane f, columns 16*(kNq0*q+j) + l) in place,
-        // one column phase at a time
-        const bool dc_row = (row & 15) == 0;
-        const float thr = P.threshold, nthr_big = -thr * 0x1p100f;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          mbar_wait(&s3done[q], ph);
-          tc_fence_after();
-          if (et == 0) stamp(P, it, 12 * p + (q == 0 ? 2 : 6));
-          if (sp == 0 && q == 0) dbg_dump(P, it, 1, p, tl + kTD2, row, 16 * G::kNq0);
-          const int ch0 = q == 0 ? 0 : G::kNq0, ch1 = q == 0 ? G::kNq0 : G::kChunks;
-          uint32_t v[2][16];
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-            if (ch0 + sp + G::kSplits * c < ch1)
-              tmem_ld16(tl + kTD2 + 16u * (ch0 + sp + G::kSplits * c), v[c]);
-          tmem_wait_ld();
-          // the packed q = 0 pairs overwrite f32 chunks other warps still read
-          if (q == 0) named_bar_sync(1, kEpiThreads);
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int ch = ch0 + sp + G::kSplits * c;
-            if (ch < ch1) {
-              const uint32_t dc = v[c][0];
-#pragma unroll
-              for (int l = 0; l < 16; ++l) {
-                const float x = __uint_as_float(v[c][l]);
-                float y;
-                // coring on the FMA pipe (the ALU pipe, 64 lanes/clk, also
-                // runs the fp16 packing): keep = sat((|x| - thr) * 2^100) is 1
-                // for |x| > thr and 0 below it (a compare + select would be
-                // two ALU instructions per coefficient)
-                if constexpr (SOFT) {
-                  const float d = fabsf(x) - thr;
-                  y = copysignf(d * __saturatef(d * 0x1p100f), x);
-                } else {
-                  y = x * __saturatef(fmaf(fabsf(x), 0x1p100f, nthr_big));
-                }
-                v[c][l] = __float_as_uint(y);
-              }
-              if (dc_row) v[c][0] = dc;  // DC coefficient kept
-              uint32_t h[8];  // fp16 pairs: the S5 A operand (K = 16 in 8 columns)
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                h[e] = pack_f16x2(__uint_as_float(v[c][2 * e]), __uint_as_float(v[c][2 * e + 1]));
-              tmem_st8(tl + kTD2 + 8u * ch, h);
-            }
-          }
-          tmem_wait_st();
-          tc_fence_before();
-          warp_arrive(&e2[q], lane);
-        }
-        if (et == 0) stamp(P, it, 12 * p + 3);
-        // ---- E3: D3 (lane f, BW columns) -> B7[f][c] fp16 (MN-major, 128B swizzle)
-        mbar_wait(s5done, ph);
-        tc_fence_after();
-        if (et == 0) stamp(P, it, 12 * p + 4);
-        if (sp == 0) dbg_dump(P, it, 2, p, tl + kTD3, row, BW);
-        {
-          uint8_t* b7 = base + kOffB7;
-          uint32_t v[2][16];
-          tmem_ld16(tl + kTD3 + 32u * sp, v[0]);
-          tmem_ld16(tl + kTD3 + 32u * sp + 16u, v[1]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {  // 8 columns = one 16-byte chunk
-            uint32_t h[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              h[e] = pack_f16x2(__uint_as_float(v[g >> 1][8 * (g & 1) + 2 * e]),
-                                __uint_as_float(v[g >> 1][8 * (g & 1) + 2 * e + 1]));
-            *reinterpret_cast<uint4*>(b7 + sw_off(row, 32 * sp + 8 * g)) =
-                make_uint4(h[0], h[1], h[2], h[3]);
-          }
-        }
-        tc_fence_before();
-        fence_proxy_async_smem();
-        warp_arrive(e3, lane);
-        if (et == 0) stamp(P, it, 12 * p + 5);
-        ph ^= 1;
+        warp_arrive(&e2[q], lane);
       }
-      // E4 of this band runs during the next band's first row phase (after
-      // its C1), off the critical path; the last band's after the loop
-      pX = X; pY = Y; pP = R.p; pit = it;
+      // ---- E3: D3 (lane f, BW columns) -> B7[i % 2][f][c] fp16 (MN-major, 128B swizzle)
+      mbar_wait(s5done, ph);
+      tc_fence_after();
+      {
+        uint8_t* b7 = base + kOffB7 + (i & 1) * G::kB7Bytes;
+        uint32_t v[2][16];
+        tmem_ld16(tl + kTD3 + 32u * sp, v[0]);
+        tmem_ld16(tl + kTD3 + 32u * sp + 16u, v[1]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int g8 = 0; g8 < 4; ++g8) {  // 8 columns = one 16-byte chunk
+          uint32_t h[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            h[e] = pack_f16x2(__uint_as_float(v[g8 >> 1][8 * (g8 & 1) + 2 * e]),
+                              __uint_as_float(v[g8 >> 1][8 * (g8 & 1) + 2 * e + 1]));
+          *reinterpret_cast<uint4*>(b7 + sw_off<128>(row, 32 * sp + 8 * g8)) =
+              make_uint4(h[0], h[1], h[2], h[3]);
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      warp_arrive(e3, lane);
+      pX = X; pY = Y; pP = gi.u.p; pi = i; pstore = !gi.warm();
     }
-    if (pit >= 0) do_e4(pit, pX, pY, pP);
+    if (pi >= 0) do_e4(pi, pX, pY, pP, pstore);
     if (et == 0) bulk_wait0();
   }
   tc_fence_before();
@@ -740,7 +767,7 @@ static cudaError_t launch_dct(const CUtensorMap& tin, const CUtensorMap& tout,
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem);
   if (e != cudaSuccess) return e;
   const int slots = G::kMinBlocks * sm_count_current();
-  const int grid = P.nregions < slots ? P.nregions : slots;
+  const int grid = P.nunits < slots ? P.nunits : slots;
   k<<<grid, G::kThreads, G::kSmem, stream>>>(tin, tout, P);
   return cudaSuccess;
 }
@@ -757,9 +784,18 @@ static ts_status dct16_run_bw(const void* in, int64_t in_rs, int64_t in_ps, void
   P.planes = planes;
   P.H = H;
   P.W = W;
-  P.nry = (H + dct::kOutRows - 1) / dct::kOutRows;
-  P.nrx = (W + G::kOutW - 1) / G::kOutW;
-  P.nregions = planes * P.nry * P.nrx;
+  P.nstrips = (W + G::kOutW - 1) / G::kOutW;
+  P.ngroups = (H + 7) / dct::kGroupOut + 1;  // the last group completes rows up to >= H
+  // whole strips when they fill the GPU twice over, else vertical segments
+  // (each after the first re-computes one warm-up group)
+  const int slots = G::kMinBlocks * sm_count_current();
+  const int64_t strips = static_cast<int64_t>(planes) * P.nstrips;
+  int nseg = strips >= 2 * slots ? 1 : static_cast<int>((2 * slots + strips - 1) / strips);
+  nseg = nseg > P.ngroups / 4 ? (P.ngroups / 4 > 1 ? P.ngroups / 4 : 1) : nseg;
+  P.seg_groups = (P.ngroups + nseg - 1) / nseg;
+  P.nseg = (P.ngroups + P.seg_groups - 1) / P.seg_groups;
+  if (strips * P.nseg > (1 << 30)) return set_error(TS_ERR_UNSUPPORTED, "dct16: too many units");
+  P.nunits = static_cast<int>(strips * P.nseg);
   P.threshold = threshold;
   P.soft = soft;
   P.consts = consts;
@@ -767,12 +803,12 @@ static ts_status dct16_run_bw(const void* in, int64_t in_rs, int64_t in_ps, void
   get_trace(&P.trace, &P.trace_ctas, &P.trace_tiles);
   CUtensorMap tin, tout;
   ts_status st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs,
-                                in_ps, 64, dct::kBandRows, CU_TENSOR_MAP_SWIZZLE_128B);
+                                in_ps, 64, dct::kGroupRows, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TS_OK) return st;
   st = encode_tmap_3d(&tout,
                       out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                      oes, out, W, H, planes, out_rs, out_ps, G::kOutW, dct::kOutRows,
+                      oes, out, W, H, planes, out_rs, out_ps, G::kOutW, dct::kGroupOut,
                       CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TS_OK) return st;
   cudaError_t e;
