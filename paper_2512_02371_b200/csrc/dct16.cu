@@ -308,7 +308,7 @@ __device__ __forceinline__ GroupIt group_next(const Params& P, GroupIt it, const
 template <int BW, typename OutT, bool SOFT, bool EPI = false>
 __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     dct16_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                 const __grid_constant__ Params P) {
+                 const __grid_constant__ CUtensorMap tm_out56, const __grid_constant__ Params P) {
   using G = Geo<BW>;
   constexpr int kEpiThreads = G::kEpiThreads;
   constexpr uint32_t kBufBytes = G::kBufBytes, kOffX = G::kOffX, kOffB7 = G::kOffB7;
@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     fence_barrier_init();
     prefetch_tmap(&tm_in);
     prefetch_tmap(&tm_out);
+    prefetch_tmap(&tm_out56);
   }
   if (warp == 1) tmem_alloc<G::kTmemCols>(tmem_slot);
   tc_fence_before();
@@ -420,8 +421,10 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + so), bx + 128u * m, id128, acc);  // hi
         mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + kStripBytes / 16 + so), bx + 128u * m, id128,
                          1u);
+#ifndef TSB_DCT_S1_TWO_TERMS
         mma_f16_ss_elect(tmem + kTD1, a_tmpl | (c4 + 2 * kStripBytes / 16 + so), bx + 128u * m,
                          id128, 1u);
+#endif
       }
       mma_commit_elect(s1done);
       mma_commit_elect(&xempty[s]);
@@ -506,8 +509,6 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         // ---- E4: D4 lanes 8 .. 71 (rows Y4 - 8 .. Y4 + 56) -> output block
         mbar_wait(s7done, i4 & 1);
         tc_fence_after();
-        if (et == 0) bulk_wait_read0();
-        named_bar_sync(1, kEpiThreads);
         uint32_t v[2][16];
         if (quarter < 3) {  // lanes 0 .. 95 (lanes >= 72 belong to no complete row)
           tmem_ld16(tl + kTD4 + 32u * sp, v[0]);
@@ -516,7 +517,10 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         }
         tc_fence_before();
         warp_arrive(e4, lane);  // D4 is free for the next group's S7
-        if (store) {
+        if (!store) return;  // a warm-up group: computed for its last tile row only
+        if (et == 0) bulk_wait_read0();  // the previous store has read the staging
+        named_bar_sync(1, kEpiThreads);
+        {
           if (row >= 8 && row < 8 + kGroupOut) {
             uint8_t* orow = base + kOffOut + (row - 8) * kOut * sizeof(OutT);
             // band columns 8..BW-9 -> output columns 0..kOut-1, 8 at a time
@@ -548,11 +552,15 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
             }
           }
         }
-        if (!store) return;  // a warm-up group: computed for its last tile row only
         fence_proxy_async_smem();
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
-          tma_store_3d(&tm_out, base + kOffOut, X4, Y4 - 8, p4);
+          // a strip's first group completes rows 0 .. 56 only (rows -8 .. 0
+          // lie above the image; TMA stores take no negative coordinates)
+          if (Y4 > 0)
+            tma_store_3d(&tm_out, base + kOffOut, X4, Y4 - 8, p4);
+          else
+            tma_store_3d(&tm_out56, base + kOffOut + 8 * kOut * sizeof(OutT), X4, 0, p4);
           bulk_commit();
         }
     };
@@ -761,14 +769,15 @@ static void build_consts(uint8_t* out) {
 
 template <int BW, typename OutT, bool SOFT, bool EPI = false>
 static cudaError_t launch_dct(const CUtensorMap& tin, const CUtensorMap& tout,
-                              const dct::Params& P, cudaStream_t stream) {
+                              const CUtensorMap& tout56, const dct::Params& P,
+                              cudaStream_t stream) {
   using G = dct::Geo<BW>;
   auto k = dct::dct16_kernel<BW, OutT, SOFT, EPI>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem);
   if (e != cudaSuccess) return e;
   const int slots = G::kMinBlocks * sm_count_current();
   const int grid = P.nunits < slots ? P.nunits : slots;
-  k<<<grid, G::kThreads, G::kSmem, stream>>>(tin, tout, P);
+  k<<<grid, G::kThreads, G::kSmem, stream>>>(tin, tout, tout56, P);
   return cudaSuccess;
 }
 
@@ -801,7 +810,7 @@ static ts_status dct16_run_bw(const void* in, int64_t in_rs, int64_t in_ps, void
   P.consts = consts;
   P.dbg = g_dct_dbg;
   get_trace(&P.trace, &P.trace_ctas, &P.trace_tiles);
-  CUtensorMap tin, tout;
+  CUtensorMap tin, tout, tout56;
   ts_status st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs,
                                 in_ps, 64, dct::kGroupRows, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TS_OK) return st;
@@ -811,24 +820,30 @@ static ts_status dct16_run_bw(const void* in, int64_t in_rs, int64_t in_ps, void
                       oes, out, W, H, planes, out_rs, out_ps, G::kOutW, dct::kGroupOut,
                       CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TS_OK) return st;
+  st = encode_tmap_3d(&tout56,
+                      out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                      oes, out, W, H, planes, out_rs, out_ps, G::kOutW, dct::kGroupOut - 8,
+                      CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st != TS_OK) return st;
   cudaError_t e;
   if (ep) {  // epilogue kernels: the default 64-column bands only (dct16_run)
     if constexpr (BW == 64) {
       if (out_dtype == TS_BF16)
-        e = soft ? launch_dct<BW, __nv_bfloat16, true, true>(tin, tout, P, stream)
-                 : launch_dct<BW, __nv_bfloat16, false, true>(tin, tout, P, stream);
+        e = soft ? launch_dct<BW, __nv_bfloat16, true, true>(tin, tout, tout56, P, stream)
+                 : launch_dct<BW, __nv_bfloat16, false, true>(tin, tout, tout56, P, stream);
       else
-        e = soft ? launch_dct<BW, float, true, true>(tin, tout, P, stream)
-                 : launch_dct<BW, float, false, true>(tin, tout, P, stream);
+        e = soft ? launch_dct<BW, float, true, true>(tin, tout, tout56, P, stream)
+                 : launch_dct<BW, float, false, true>(tin, tout, tout56, P, stream);
     } else {
       return set_error(TS_ERR_UNSUPPORTED, "dct16: output epilogue needs 64-column bands");
     }
   } else if (out_dtype == TS_BF16) {
-    e = soft ? launch_dct<BW, __nv_bfloat16, true>(tin, tout, P, stream)
-             : launch_dct<BW, __nv_bfloat16, false>(tin, tout, P, stream);
+    e = soft ? launch_dct<BW, __nv_bfloat16, true>(tin, tout, tout56, P, stream)
+             : launch_dct<BW, __nv_bfloat16, false>(tin, tout, tout56, P, stream);
   } else {
-    e = soft ? launch_dct<BW, float, true>(tin, tout, P, stream)
-             : launch_dct<BW, float, false>(tin, tout, P, stream);
+    e = soft ? launch_dct<BW, float, true>(tin, tout, tout56, P, stream)
+             : launch_dct<BW, float, false>(tin, tout, tout56, P, stream);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "dct16 launch");
