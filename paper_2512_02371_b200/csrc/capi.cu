@@ -126,7 +126,7 @@ ts_status ts_axis_pass_ep(const ts_axis* a, int dim, int planes, int height, int
 }
 
 #ifdef TSB_DIAG
-ts_status ts_debug_trace(void* device_buffer, int ctas, int tiles) {
+TS_API ts_status ts_debug_trace(void* device_buffer, int ctas, int tiles) {
   if (device_buffer && (ctas < 1 || tiles < 1))
     return set_error(TS_ERR_INVALID, "trace: ctas and tiles must be >= 1");
   set_trace(device_buffer, ctas, tiles);

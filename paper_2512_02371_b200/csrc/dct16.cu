@@ -125,7 +125,7 @@ struct Params {
   float threshold;
   int soft;                 // 0 hard, 1 soft coring
   const uint8_t* consts;    // kConstBytes
-  float* dbg;               // diagnostics: [4 stages][2 phases][128 lanes][256] for CTA 0, band 0
+  float* dbg;               // diagnostics (TSB_DIAG): forward coefficients, (planes, ty, tx, 16, 16) f32
   unsigned long long* trace;  // diagnostics (ts_debug_trace): clock64 per (CTA, band, event), 24 events
   int trace_ctas, trace_tiles;
   EpiK ep;  // output epilogue (EPI kernels only)
@@ -138,21 +138,6 @@ __device__ __forceinline__ void stamp(const Params& P, int it, int ev) {
 #ifdef TSB_DIAG
   if (P.trace != nullptr && static_cast<int>(blockIdx.x) < P.trace_ctas && it < P.trace_tiles)
     P.trace[(static_cast<size_t>(blockIdx.x) * P.trace_tiles + it) * 24 + ev] = clock64();
-#endif
-}
-
-// Diagnostics: copy `ncols` TMEM columns of this thread's lane to dbg.
-__device__ __forceinline__ void dbg_dump(const Params& P, int it, int stage, int p, uint32_t taddr,
-                                         int row, int ncols) {
-#ifdef TSB_DIAG
-  if (P.dbg == nullptr || blockIdx.x != 0 || it != 0) return;
-  float* dst = P.dbg + ((static_cast<size_t>(stage) * 2 + p) * 128 + row) * 256;
-  for (int c0 = 0; c0 < ncols; c0 += 16) {
-    uint32_t r[16];
-    tmem_ld16(taddr + c0, r);
-    tmem_wait_ld();
-    for (int i = 0; i < 16; ++i) dst[c0 + i] = __uint_as_float(r[i]);
-  }
 #endif
 }
 
@@ -609,6 +594,19 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
           if (ch0 + sp + G::kSplits * c < ch1)
             tmem_ld16(tl + kTD2 + 16u * (ch0 + sp + G::kSplits * c), v[c]);
         tmem_wait_ld();
+#ifdef TSB_DIAG
+        if (P.dbg != nullptr) {  // every forward coefficient, laid out like the oracle's
+          const int ty = P.H / 8 + 1, tx = P.W / 8 + 1, t = 8 * gi.g + (row >> 4);
+          for (int c = 0; c < 2; ++c) {
+            const int ch = ch0 + sp + G::kSplits * c;
+            const int u = X / 8 + 2 * (q ? ch - G::kNq0 : ch) + q;
+            if (ch < ch1 && t < ty && u < tx)
+              for (int l = 0; l < 16; ++l)
+                P.dbg[((((static_cast<size_t>(gi.u.p) * ty + t) * tx + u) * 16 + (row & 15)) * 16) + l] =
+                    __uint_as_float(v[c][l]);
+          }
+        }
+#endif
         // the packed q = 0 pairs overwrite f32 chunks other warps still read
         if (q == 0) named_bar_sync(1, kEpiThreads);
 #pragma unroll

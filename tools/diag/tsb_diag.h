@@ -18,9 +18,11 @@ extern "C" {
 
 #define TS_DIAG_API TS_API
 
-/* Diagnostics: subsequent ts_denoise_dct16 launches copy the TMEM
- * accumulators of CTA 0's first band (D1, D2, D3 per phase; D4) into
- * device_buffer (f32[4][2][128][256]); NULL turns it off. */
+/* Diagnostics: subsequent ts_denoise_dct16 launches also write every
+ * forward coefficient (before coring, f32) into device_buffer, laid out like
+ * oracle/pipelines_ref.dct_coefficients: (planes, H/8 + 1, W/8 + 1, 16, 16)
+ * (tile row, tile column, row frequency, column frequency).  NULL turns it
+ * off.  Measures the forward chain's error (tools/dct_coef_error.py). */
 TS_DIAG_API ts_status ts_debug_dct16(float* device_buffer);
 
 /* Diagnostics: make subsequent ts_separable_run launches record clock64()
