@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 1
+#define TS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define TS_API __attribute__((visibility("default")))
@@ -223,6 +223,19 @@ typedef struct ts_conv_group {
   /* device int32[3], zeroed by the caller: on an out-of-bounds read the
    * first failing thread writes {1 (src) | 2 (kern), index, iteration}. */
   int32_t* error;
+  /* ABI 2, optional.  Compact explicit gathers: when a_shift is non-NULL,
+   * a_idx / b_idx hold ONE [m*n][k] table shared by every iteration, and
+   * iteration v reads src index a_idx[..] + a_shift[v]. */
+  const int32_t* a_shift;
+  /* ABI 2, optional.  Independent iterations (a For loop whose body is
+   * zero-fill, one conv statement, then a copy or wmma_store of the result):
+   * when out_base is non-NULL every iteration starts from 0 and stores its
+   * m*n results at out[t*out_stride + out_base[v] + out_off[o]] (out_off NULL
+   * = o); acc is not touched.  All iterations run in parallel. */
+  const int32_t* out_base;
+  const int32_t* out_off;
+  float* out;
+  int64_t out_stride;
 } ts_conv_group;
 
 /* Replaces the serial For/Store walk of interp.run_program (interp.py:570-619)

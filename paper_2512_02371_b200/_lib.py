@@ -19,6 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TSB_LIB_PATH") or os.path.join(_HERE, "_native", "libtsb200.so")
 
 TS_BF16, TS_F32, TS_F16 = 1, 2, 3
+ABI_VERSION = 2  # include/tensorsel_b200.h TS_ABI_VERSION
 TS_AXIS_DC_EXACT = 0x1
 
 _lock = threading.Lock()
@@ -40,6 +41,9 @@ class ConvGroup(ctypes.Structure):
         ("a_base", ctypes.c_void_p), ("k_base", ctypes.c_void_p), ("b_off", ctypes.c_void_p),
         ("a_idx", ctypes.c_void_p), ("b_idx", ctypes.c_void_p),
         ("error", ctypes.c_void_p),
+        ("a_shift", ctypes.c_void_p),
+        ("out_base", ctypes.c_void_p), ("out_off", ctypes.c_void_p),
+        ("out", ctypes.c_void_p), ("out_stride", ctypes.c_int64),
     ]
 
 
@@ -131,7 +135,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ts_abi_version() != 1:
+        if lib.ts_abi_version() != ABI_VERSION:
             raise NativeLibraryMissing(f"ABI mismatch: library reports {lib.ts_abi_version()}")
         if path is None:
             _lib = lib

@@ -365,7 +365,65 @@ def _compile(p, extra_shapes, strict):
 
     for i, st in enumerate(p.body):
         emit_stmt(st, {}, f"body[{i}]")
+    plan.ops = _fuse_independent_iterations(plan.ops)
     return plan
+
+
+def _fuse_independent_iterations(ops):
+    """Peephole over the unrolled plan: a run of For iterations whose body is
+    ``acc = 0; acc = conv(...) + acc; out[base_v ..] = acc`` (copy or
+    wmma_store) becomes ONE ("scatter", ...) op — every iteration computed
+    from zero in parallel and stored to its own slot, then acc set to the
+    last iteration's value (the reference's final buffer state).  Each
+    iteration's arithmetic is unchanged (0 + s, interp.py:485 / 270-284)."""
+    out, i = [], 0
+    while i < len(ops):
+        run = []
+        j = i
+        while j + 2 < len(ops):
+            f, g, c = ops[j], ops[j + 1], ops[j + 2]
+            if f[0] not in ("fill", "zero") or (f[0] == "fill" and f[2] != 0.0):
+                break
+            if g[0] != "group" or len(g[2].a_base) != 1:
+                break
+            grp = g[2]
+            acc, n = f[1], f[-1]
+            if grp.acc != acc or grp.m * grp.n != n or acc in (grp.src, grp.kern):
+                break
+            if c[1] in (grp.src, grp.kern):  # an iteration would read an earlier one's output
+                break
+            if c[0] == "copy" and c[2] == acc and c[3] == n and c[5] == 0 and c[1] != acc:
+                dst, base, off = c[1], c[4], None
+            elif c[0] == "store" and c[2] == acc and c[4] == n and c[1] != acc \
+                    and len(np.unique(c[3])) == n:
+                dst, base, off = c[1], int(c[3][0]), np.asarray(c[3], np.int64) - int(c[3][0])
+            else:
+                break
+            if run:
+                k0, g0, d0, o0 = run[0][1], run[0][2], run[0][3], run[0][5]
+                if g[1] != k0 or dst != d0 or acc != g0.acc or \
+                        (off is None) != (o0 is None) or (off is not None and
+                                                          not np.array_equal(off, o0)):
+                    break
+            run.append((f, g[1], grp, dst, base, off))
+            j += 3
+        if len(run) >= 2:
+            g0 = run[0][2]
+            G = _Group(g0.acc, g0.src, g0.kern, g0.m, g0.k, g0.n)
+            G.a_stride, G.b_off, G.tmp = g0.a_stride, g0.b_off, g0.tmp
+            for _, _, grp, _, _, _ in run:
+                G.a_base += grp.a_base
+                G.k_base += grp.k_base
+                G.a_idx += grp.a_idx
+                G.b_idx += grp.b_idx
+                G.paths += grp.paths
+            out.append(("scatter", run[0][1], G, run[0][3], [r[4] for r in run], run[0][5],
+                        g0.m * g0.n))
+            i = j
+        else:
+            out.append(ops[i])
+            i += 1
+    return out
 
 
 def _append_iteration(plan, key, acc, src, kbuf, m, k, n, a_stride, a_base, k_base, off, tmp, sp):
@@ -517,6 +575,13 @@ def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=N
             bufs[out][:, torch.from_numpy(idx).to(dev)] = bufs[tile][:, src_pos]
         elif kind == "group":
             _run_group(lib, op[2], bufs, meta, T, dev, stream, err)
+        elif kind == "scatter":
+            _, _, g, dst, bases, off, n = op
+            _run_group(lib, g, bufs, meta, T, dev, stream, err, scatter=(dst, bases, off))
+            # the accumulator ends holding the last iteration's result
+            last = bases[-1] + (torch.from_numpy(off).to(dev) if off is not None
+                                else torch.arange(n, device=dev))
+            bufs[g.acc][:, :n] = bufs[dst][:, last]
         else:
             raise UnknownIntrinsic(kind)
     torch.cuda.synchronize(dev)
@@ -531,7 +596,21 @@ def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=N
     return out
 
 
-def _run_group(lib, g, bufs, meta, T, dev, stream, err):
+def _compact(a_idx, b_idx):
+    """(table, b table, per-iteration shifts) when every iteration's gather
+    is the first one shifted by a constant (e.g. a For loop sliding a conv
+    window), else None."""
+    A = np.stack(a_idx)
+    shifts = A[:, :1, :1] - A[:1, :1, :1]
+    if not np.array_equal(A - shifts, np.broadcast_to(A[:1], A.shape)):
+        return None
+    B = np.stack(b_idx)
+    if not np.array_equal(B, np.broadcast_to(B[:1], B.shape)):
+        return None
+    return A[0], B[0], shifts.reshape(-1)
+
+
+def _run_group(lib, g, bufs, meta, T, dev, stream, err, scatter=None):
     import torch
     src, kern, acc = bufs[g.src], bufs[g.kern], bufs[g.acc]
     V = len(g.a_base)
@@ -554,11 +633,22 @@ def _run_group(lib, g, bufs, meta, T, dev, stream, err):
     c.m, c.k, c.n, c.a_stride = g.m, g.k, g.n, g.a_stride
     c.iterations = V
     if g.a_idx:
-        c.a_idx = dptr(np.stack(g.a_idx))
-        c.b_idx = dptr(np.stack(g.b_idx))
+        comp = _compact(g.a_idx, g.b_idx) if V > 1 else None
+        if comp is not None:  # one gather table + a shift per iteration
+            c.a_idx, c.b_idx, c.a_shift = dptr(comp[0]), dptr(comp[1]), dptr(comp[2])
+        else:
+            c.a_idx = dptr(np.stack(g.a_idx))
+            c.b_idx = dptr(np.stack(g.b_idx))
     else:
         c.a_base, c.k_base = dptr(g.a_base), dptr(g.k_base)
         c.b_off = dptr(g.b_off)
+    if scatter is not None:
+        dst, bases, off = scatter
+        out = bufs[dst]
+        c.out, c.out_stride = out.data_ptr(), out.shape[1]
+        c.out_base = dptr(bases)
+        if off is not None:
+            c.out_off = dptr(off)
     err.zero_()
     c.error = err.data_ptr()
     _lib.check(lib.ts_run_conv_group(ctypes.byref(c), stream), "ts_run_conv_group")

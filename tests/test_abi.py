@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(_lib.EXPORTED)
-    assert lib.ts_abi_version() == 1
+    assert lib.ts_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_device_count_is_callable():

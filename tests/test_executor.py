@@ -127,3 +127,19 @@ def test_gpu_batched_difftest_many_seeds(programs):
     b = executor.run_program_batch(low, ins)
     for x, y in zip(a, b):
         assert x["output"].data.tobytes() == y["output"].data.tobytes()
+
+
+def test_for_loop_of_independent_conv_windows_fuses_to_one_launch():
+    """A For loop whose body is fill / conv / copy-out (the image-scale
+    generated program of tests/test_cli.py) compiles to ONE scatter op with
+    every iteration, instead of 3 ops per iteration; its gathers compact to
+    one table plus a shift per iteration."""
+    from test_cli import _lanczos_stream_program
+    plan = executor._compile(irlite.parse_program(_lanczos_stream_program(64)), (), False)
+    kinds = [o[0] for o in plan.ops]
+    assert kinds.count("scatter") == 1 and "copy" not in kinds, kinds
+    op = next(o for o in plan.ops if o[0] == "scatter")
+    g = op[2]
+    assert len(g.a_base) == 64 and op[4] == [256 * t for t in range(64)]
+    table, btable, shifts = executor._compact(g.a_idx, g.b_idx)
+    assert table.shape == (256, 12) and list(shifts[:3]) == [0, 512, 1024]
