@@ -369,6 +369,29 @@ def _compile(p, extra_shapes, strict):
     return plan
 
 
+_PLANS: "dict" = {}
+_PLANS_MAX = 64
+
+
+def _compiled(p, extra_shapes, strict):
+    """_compile, cached per (program, extra_shapes, strict): programs are
+    immutable (frozen dataclasses, here and in tensorsel.ir), and a plan
+    only depends on the program, so repeated runs (difftest trials, batches
+    of frames) skip the host-side unrolling."""
+    try:
+        key = (p, tuple(extra_shapes), bool(strict))
+        hash(key)
+    except TypeError:
+        return _compile(p, extra_shapes, strict)
+    plan = _PLANS.get(key)
+    if plan is None:
+        plan = _compile(p, extra_shapes, strict)
+        if len(_PLANS) >= _PLANS_MAX:
+            _PLANS.pop(next(iter(_PLANS)))
+        _PLANS[key] = plan
+    return plan
+
+
 def _fuse_independent_iterations(ops):
     """Peephole over the unrolled plan: a run of For iterations whose body is
     ``acc = 0; acc = conv(...) + acc; out[base_v ..] = acc`` (copy or
@@ -514,7 +537,7 @@ def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=N
     dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
     lib = _lib.load()
     T = len(inputs_list)
-    plan = _compile(p, extra_shapes, strict)
+    plan = _compiled(p, extra_shapes, strict)
     bufs, meta = {}, {}
     for prm in p.params:
         if prm.kind == "i32":
