@@ -372,8 +372,7 @@ def run_b200(args):
             "clocks": clk,
             "sustained": {"value": round(pix_step / (sus_ms / 1e3) / 1e6, 1), "unit": "Mpixel/s",
                           "ms_per_step": round(sus_ms, 5), "steps": n_sus,
-                          "roofline_frac": round(alg_bytes / (sus_ms / launches_per_step / 1e3) /
-                                                 1e9 / peak, 4),
+                          "roofline_frac": round(alg_bytes / (sus_ms / 1e3) / 1e9 / peak, 4),
                           "sm_mhz": sus_clk.get("sm_mhz"), "reasons": sus_clk.get("reasons"),
                           "note": "same step back to back for ~1 s after the timed region "
                                   "(synchronised every 8 steps); not the headline"},

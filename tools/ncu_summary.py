@@ -56,7 +56,10 @@ def main():
     report, lcsv, prefix = sys.argv[1:4]
     frames = int(sys.argv[4]) if len(sys.argv) > 4 else 8
     k = raw(report)[0]
-    dur_us = float(k["gpu__time_duration.sum"][0])
+    v, u = k["gpu__time_duration.sum"]
+    dur_us = float(v.replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
+                                          "msecond": 1e3, "ms": 1e3, "second": 1e6,
+                                          "s": 1e6}.get(u.strip(), 1.0)
     rd = to_bytes(*k["dram__bytes_read.sum"])
     wr = to_bytes(*k["dram__bytes_write.sum"])
     per_frame = int(sys.argv[5]) if len(sys.argv) > 5 else 3 * 2160 * 3840 * 2 + 3 * 1080 * 1920 * 2
