@@ -490,9 +490,16 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t tl = tmem + lane_off;
     const int et = threadIdx.x - 64;
+    // one warp polls each MMA-completion barrier; the other epilogue warps
+    // block in a hardware named barrier, which issues nothing (polling
+    // waiters were ~18% of the kernel's instructions; 0.7% faster)
+    auto ewait = [&](uint64_t* bar, uint32_t parity) {
+      if (warp == 2) mbar_wait(bar, parity);
+      named_bar_sync(2, kEpiThreads);
+    };
     auto do_e4 = [&](int i4, int X4, int Y4, int p4, bool store) {
         // ---- E4: D4 lanes 8 .. 71 (rows Y4 - 8 .. Y4 + 56) -> output block
-        mbar_wait(s7done, i4 & 1);
+        ewait(s7done, i4 & 1);
         tc_fence_after();
         uint32_t v[2][16];
         if (quarter < 3) {  // lanes 0 .. 95 (lanes >= 72 belong to no complete row)
@@ -556,7 +563,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       const uint32_t ph = i & 1;
       const int Y = kGroupOut * gi.g, X = gi.u.sx * kOut;
       // ---- C1: D1 (f32, lane f, BW columns) -> fp16 hi/lo pairs: hi at [0, BW/2), lo at [BW/2, BW)
-      mbar_wait(s1done, ph);
+      ewait(s1done, ph);
       tc_fence_after();
       {
         uint32_t v[2][16];
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       const float thr = P.threshold, nthr_big = -thr * 0x1p100f;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        mbar_wait(&s3done[q], ph);
+        ewait(&s3done[q], ph);
         tc_fence_after();
         const int ch0 = q == 0 ? 0 : G::kNq0, ch1 = q == 0 ? G::kNq0 : G::kChunks;
         uint32_t v[2][16];
@@ -642,7 +649,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         warp_arrive(&e2[q], lane);
       }
       // ---- E3: D3 (lane f, BW columns) -> B7[i % 2][f][c] fp16 (MN-major, 128B swizzle)
-      mbar_wait(s5done, ph);
+      ewait(s5done, ph);
       tc_fence_after();
       {
         uint8_t* b7 = base + kOffB7 + (i & 1) * G::kB7Bytes;
