@@ -67,6 +67,14 @@ void get_trace(unsigned long long** buf, int* ctas, int* tiles);
 
 namespace dct {
 
+// polling back-off (ns) of the loader's and the MMA issuer's waits
+#ifndef TSB_DCT_LOADER_NS
+#define TSB_DCT_LOADER_NS 256
+#endif
+#ifndef TSB_DCT_MMA_NS
+#define TSB_DCT_MMA_NS 32
+#endif
+
 // constants (built on the host, one bulk copy per CTA):
 //   S1 strip : hi, lo: 256 rows x 16 K, K-major core matrices (8192 B each)
 //   S7 strip : 248 rows x 16 K
@@ -365,7 +373,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       const Unit& U = gi.u;
       uint8_t* dst = base + kOffX + s * kBufBytes;
       if (lane == 0) {
-        mbar_wait(&xempty[s], ((i / kNX) & 1) ^ 1);
+        mbar_wait_backoff(&xempty[s], ((i / kNX) & 1) ^ 1, TSB_DCT_LOADER_NS);
         mbar_arrive_expect_tx(&xfull[s], kBufBytes);
 #pragma unroll
         for (int h = 0; h < BW / 64; ++h)
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       const uint32_t ph = i & 1;
       const GroupIt nx = group_next(P, gi, ustep);
       // ---- S3: row forward, A = packed D1 from TMEM
-      mbar_wait(c1, ph);
+      mbar_wait_backoff(c1, ph, TSB_DCT_MMA_NS);
       tc_fence_after();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       }
       // ---- S5: row inverse (TS f16, A = cored D2 packed at kTD2 + 8 ch) into
       // D3, which overlays the q = 1 f32 chunks: after all of E2
-      mbar_wait(&e2[1], ph);
+      mbar_wait_backoff(&e2[1], ph, TSB_DCT_MMA_NS);
       tc_fence_after();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -458,13 +466,13 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
                            b5, id16h, q > 0 ? 1u : 0u);
       }
       mma_commit_elect(s5done);
-      mbar_wait(e3, ph);
+      mbar_wait_backoff(e3, ph, TSB_DCT_MMA_NS);
       // ---- S7: column inverse, D4 = Σ_k T_kᵀ · B7_k (fp16); D4 lane r =
       // input row 64g - 16 + r.  Tile k (k = -1 .. 7, -1 = the previous
       // group's last tile, still in the other B7 buffer) covers lanes
       // 8k + 8 .. 8k + 24, so lanes 8 .. 71 (rows 64g - 8 .. 64g + 56) are
       // complete: no row halo is recomputed between groups.
-      if (i > 0) mbar_wait(e4, (i - 1) & 1);  // the previous group's E4 has read D4
+      if (i > 0) mbar_wait_backoff(e4, (i - 1) & 1, TSB_DCT_MMA_NS);  // the previous group's E4 has read D4
       tc_fence_after();
       const bool prev = !gi.first();  // the group above is this unit's, in the other B7
       if (prev)

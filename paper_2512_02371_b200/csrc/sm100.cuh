@@ -103,6 +103,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// mbar_wait for a single-warp role (loader, MMA issuer) whose waits are long:
+// between polls the warp sleeps `ns` nanoseconds, so it does not take the
+// issue slots of the warps doing the work it waits for.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = global_timer_ns();
+  for (;;) {
+#pragma unroll 1
+    for (int i = 0; i < 1024; ++i) {
+      if (mbar_try_wait(bar, parity)) return;
+      __nanosleep(ns);
+    }
+    if (global_timer_ns() - t0 > 4000000000ull) __trap();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // fences / named barriers
 
