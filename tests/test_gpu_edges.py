@@ -173,3 +173,19 @@ def test_output_epilogue_clamp_and_normalise(case):
         b = fnn(out_dtype=dt, clamp=(0.0, 1.0))
         assert torch.equal(torch.isnan(a), torch.isnan(b))
         assert torch.isnan(b).any()
+
+
+def test_f32_kernel_more_planes_than_a_grid_dimension():
+    """70000 tiny f32 planes (> 65535, the old grid.z limit): the persistent
+    f32 kernel walks them all, bit-exact in exact mode."""
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    x = torch.from_numpy(np.random.default_rng(38).random((70000, 8, 16), dtype=np.float32))
+    exact, pipelines.F32_EXACT = pipelines.F32_EXACT, True
+    try:
+        y = pipelines.resample(x.cuda(), 4, 8, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+    finally:
+        pipelines.F32_EXACT = exact
+    ref = pipelines_ref.resample(x.numpy(), 4, 8)
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), ref.view(np.uint32))
