@@ -278,7 +278,7 @@ def run_b200(args):
         # pipelines.run_from_host overlaps H2D / kernels / D2H over 3 streams
         for c in range(n_chunks):
             n = min(ch, F - c * ch) * 3
-            _pipes.run_from_host(fn, host_in[:n], host_out[:n], chunk_planes=12)
+            _pipes.run_from_host(fn, host_in[:n], host_out[:n], chunk_planes=3)
 
     E = max(1, min(args.e2e_steps, K))
     for _ in range(2):

@@ -354,7 +354,7 @@ extern "C" ts_status ts_separable_f32_ep(int planes, const float* in, int in_h, 
                                          int64_t out_row_stride, int64_t out_plane_stride,
                                          int out_dtype, int flags, const ts_epilogue* ep,
                                          void* stream) {
-  if (planes < 0 || in_h < 1 || in_w < 1 || out_h < 1 || out_w < 1 || planes > 65535)
+  if (planes < 0 || in_h < 1 || in_w < 1 || out_h < 1 || out_w < 1)
     return set_error(TS_ERR_INVALID, "separable_f32: bad sizes");
   if (planes == 0) return TS_OK;
   if (!in || !out || !row_weights || !col_weights)

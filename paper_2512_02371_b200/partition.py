@@ -149,7 +149,7 @@ class FrameSharder:
 
 
 def run_sharded(fn, host_in, host_out, devices, *, planes_per_frame: int = 3,
-                chunk_planes: int = 12):
+                chunk_planes: int = 3):
     """Run `fn` (a pipeline of :mod:`pipelines`) over a batch of frames held in
     (pinned) host memory on several devices from ONE process: frame shards
     (:func:`frame_shard`) go to ``devices`` in order, each streamed through

@@ -312,7 +312,7 @@ def separable(x, rows: "_axis.Axis", cols: "_axis.Axis", *, out_dtype=None, clam
 _LANES = {}
 
 
-def run_from_host(fn, host_in, host_out, *, chunk_planes: int = 12, lanes: int = 3):
+def run_from_host(fn, host_in, host_out, *, chunk_planes: int = 3, lanes: int = 3):
     """Stream a batch of planes from (pinned) host memory through `fn` (any
     pipeline of this module) and back: chunks of `chunk_planes` planes rotate
     over `lanes` CUDA streams, so the host->device copy of one chunk, the
