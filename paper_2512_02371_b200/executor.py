@@ -307,14 +307,22 @@ def _compile(p, extra_shapes, strict):
             # operand A: src[a_base + i*a_stride + kk] (interp._tile_gather, interp.py:408-410)
             rows_off = a_stride * np.arange(m)
             check_range(src, a_base + int(rows_off.min()), a_base + int(rows_off.max()) + k - 1)
-            if bk != k or b_base != 0 or b_stride != bn:
-                raise UnsupportedProgram("wmma_load_b must read the whole temporary row-major")
-            if tmp not in tmp_defs:
-                raise UnsupportedProgram(f"B operand {tmp!r} is not a weight temporary")
-            check_range(tmp, 0, k * bn - 1)
-            kbuf, kb, off = tmp_defs[tmp]
-            if len(off) != k * bn:
-                raise EvalError(f"temporary {tmp!r} has {len(off)} lanes, B needs {k * bn}")
+            if bk != k:
+                raise UnsupportedProgram("wmma_load_b rows must equal wmma_load_a columns")
+            if tmp in tmp_defs:  # B = a Toeplitz temporary (conv-toeplitz / upsample-polyphase)
+                if b_base != 0 or b_stride != bn:
+                    raise UnsupportedProgram("wmma_load_b must read the whole temporary row-major")
+                check_range(tmp, 0, k * bn - 1)
+                kbuf, kb, off = tmp_defs[tmp]
+                if len(off) != k * bn:
+                    raise EvalError(f"temporary {tmp!r} has {len(off)} lanes, B needs {k * bn}")
+            else:
+                # B = a plain buffer tile (the wmma-mma rule's matmul form,
+                # rules.py:904-1008): B[b_base + b_stride*r + c], r < k, c < n
+                off = (b_stride * np.arange(k)[:, None] + np.arange(bn)[None, :]).reshape(-1)
+                check_range(tmp, b_base + int(off.min()), b_base + int(off.max()))
+                kbuf, kb, off = tmp, b_base, off.astype(np.int32)
+                tmp = None  # nothing to materialise
             if _cls(lc) == "Load" and lc.buffer == s.buffer and _is_flat(lc.index, m * bn):
                 check_range(s.buffer, 0, m * bn - 1)
             elif _cls(lc) == "Call" and lc.name == "wmma_zero":

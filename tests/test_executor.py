@@ -143,3 +143,52 @@ def test_for_loop_of_independent_conv_windows_fuses_to_one_launch():
     assert len(g.a_base) == 64 and op[4] == [256 * t for t in range(64)]
     table, btable, shifts = executor._compact(g.a_idx, g.b_idx)
     assert table.shape == (256, 12) and list(shifts[:3]) == [0, 512, 1024]
+
+
+def mm_program_text(n_tiles, fixed_left):
+    """The DCT fixture programs of oracle/make_golden.py (mm_program): C_t =
+    A_t · B_t for n_tiles 16x16 tiles, wmma_load_a / wmma_load_b of plain
+    buffers (the wmma-mma rule's matmul form, rules.py:904-1008)."""
+    R = "(ramp (imm i32 0) (imm i32 1) 256)"
+    base = "(mul (var t) (imm i32 256))"
+    a_len, b_len = (256, 256 * n_tiles) if fixed_left else (256 * n_tiles, 256)
+    a_base, b_base = ("(imm i32 0)", base) if fixed_left else (base, "(imm i32 0)")
+    return (f"(param A f32 {a_len} mem)\n(param B f32 {b_len} mem)\n"
+            f"(param O f32 {256 * n_tiles} mem)\n(wmma-shape 16 16 16)\n"
+            f"(allocate acc f32 256 wmma)\n"
+            f"(for t 0 {n_tiles}\n"
+            f" (store acc {R} (call wmma_zero (imm i32 16) (imm i32 16)))\n"
+            f" (store acc {R} (call wmma_mma (call wmma_load_a (var A) {a_base} (imm i32 16) "
+            f"(imm i32 16) (imm i32 16)) (call wmma_load_b (var B) {b_base} (imm i32 16) "
+            f"(imm i32 16) (imm i32 16)) (load acc (f32 256) {R})))\n"
+            f" (evaluate (call wmma_store (var O) {base} (imm i32 16) (imm i32 16) "
+            f"(load acc (f32 256) {R}))))\n")
+
+
+def test_plain_buffer_matmul_compiles_to_one_scatter():
+    plan = executor._compile(irlite.parse_program(mm_program_text(12, True)), (), True)
+    kinds = [o[0] for o in plan.ops]
+    assert kinds.count("scatter") == 1, kinds
+    g = next(o for o in plan.ops if o[0] == "scatter")[2]
+    assert len(g.a_base) == 12 and g.k_base[:3] == [0, 256, 512] and g.tmp is None
+
+
+@pytest.mark.gpu
+def test_dct_fixture_programs_run_bit_exactly_on_the_gpu(G):
+    """The four 16x16x16 products per tile of the DCT fixture, run as the
+    same wmma programs the reference ran (oracle/make_golden.py) through the
+    GPU executor: the forward coefficients equal the reference's bit for
+    bit."""
+    Dw = G["dct_Dw"]
+    want = G["dct_coeffs"]
+    P, ty, tx = want.shape[:3]
+    n = P * ty * tx
+    import oracle.pipelines_ref as R
+    T = R.dct_tiles(G["dct_img"]).reshape(n, 16, 16)
+    left = irlite.parse_program(mm_program_text(n, True))
+    right = irlite.parse_program(mm_program_text(n, False))
+    P1 = executor.run_program(left, {"A": Dw.reshape(-1), "B": T.reshape(-1),
+                                     "O": np.zeros(256 * n, np.float32)}, strict=True)["O"].data
+    C = executor.run_program(right, {"A": P1, "B": np.ascontiguousarray(Dw.T).reshape(-1),
+                                     "O": np.zeros(256 * n, np.float32)}, strict=True)["O"].data
+    assert C.tobytes() == want.astype(np.float32).tobytes()
