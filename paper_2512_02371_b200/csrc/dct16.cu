@@ -145,7 +145,7 @@ struct Params {
 __device__ __forceinline__ void stamp(const Params& P, int it, int ev) {
 #ifdef TSB_DIAG
   if (P.trace != nullptr && static_cast<int>(blockIdx.x) < P.trace_ctas && it < P.trace_tiles)
-    P.trace[(static_cast<size_t>(blockIdx.x) * P.trace_tiles + it) * 24 + ev] = clock64();
+    P.trace[(static_cast<size_t>(blockIdx.x) * P.trace_tiles + it) * 16 + ev] = clock64();
 #endif
 }
 
@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       // ---- S3: row forward, A = packed D1 from TMEM
       mbar_wait_backoff(c1, ph, TSB_DCT_MMA_NS);
       tc_fence_after();
+      if (lane == 0) stamp(P, i, 9);  // S3 issue
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
 #pragma unroll
@@ -458,6 +459,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       // D3, which overlays the q = 1 f32 chunks: after all of E2
       mbar_wait_backoff(&e2[1], ph, TSB_DCT_MMA_NS);
       tc_fence_after();
+      if (lane == 0) stamp(P, i, 10);  // S5 issue
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
 #pragma unroll
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       }
       mma_commit_elect(s5done);
       mbar_wait_backoff(e3, ph, TSB_DCT_MMA_NS);
+      if (lane == 0) stamp(P, i, 11);  // E3 seen
       // ---- S7: column inverse, D4 = Σ_k T_kᵀ · B7_k (fp16); D4 lane r =
       // input row 64g - 16 + r.  Tile k (k = -1 .. 7, -1 = the previous
       // group's last tile, still in the other B7 buffer) covers lanes
@@ -474,6 +477,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       // complete: no row halo is recomputed between groups.
       if (i > 0) mbar_wait_backoff(e4, (i - 1) & 1, TSB_DCT_MMA_NS);  // the previous group's E4 has read D4
       tc_fence_after();
+      if (lane == 0) stamp(P, i, 12);  // S7 issue
       const bool prev = !gi.first();  // the group above is this unit's, in the other B7
       if (prev)
         mma_f16_ss_elect(tmem + kTD4, a_tmpl | (c4 + kCS7 / 16 + 15u * 16u),
@@ -509,6 +513,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         // ---- E4: D4 lanes 8 .. 71 (rows Y4 - 8 .. Y4 + 56) -> output block
         ewait(s7done, i4 & 1);
         tc_fence_after();
+        if (et == 0) stamp(P, i4, 7);  // D4 seen
         uint32_t v[2][16];
         if (quarter < 3) {  // lanes 0 .. 95 (lanes >= 72 belong to no complete row)
           tmem_ld16(tl + kTD4 + 32u * sp, v[0]);
@@ -517,6 +522,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         }
         tc_fence_before();
         warp_arrive(e4, lane);  // D4 is free for the next group's S7
+        if (et == 0) stamp(P, i4, 8);  // D4 read
         if (!store) return;  // a warm-up group: computed for its last tile row only
         if (et == 0) bulk_wait_read0();  // the previous store has read the staging
         named_bar_sync(1, kEpiThreads);
@@ -573,6 +579,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       // ---- C1: D1 (f32, lane f, BW columns) -> fp16 hi/lo pairs: hi at [0, BW/2), lo at [BW/2, BW)
       ewait(s1done, ph);
       tc_fence_after();
+      if (et == 0) stamp(P, i, 0);  // D1 seen
       {
         uint32_t v[2][16];
         tmem_ld16(tl + kTD1 + 32u * sp, v[0]);
@@ -590,6 +597,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       tmem_wait_st();
       tc_fence_before();
       warp_arrive(c1, lane);
+      if (et == 0) stamp(P, i, 1);  // C1 done
       if (pi >= 0) {  // the previous group's E4, off the critical path
         do_e4(pi, pX, pY, pP, pstore);
         pi = -1;
@@ -602,6 +610,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       for (int q = 0; q < 2; ++q) {
         ewait(&s3done[q], ph);
         tc_fence_after();
+        if (et == 0) stamp(P, i, 2 + q);  // D2 phase q seen
         const int ch0 = q == 0 ? 0 : G::kNq0, ch1 = q == 0 ? G::kNq0 : G::kChunks;
         uint32_t v[2][16];
 #pragma unroll
@@ -656,9 +665,11 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
         tc_fence_before();
         warp_arrive(&e2[q], lane);
       }
+      if (et == 0) stamp(P, i, 4);  // E2 done
       // ---- E3: D3 (lane f, BW columns) -> B7[i % 2][f][c] fp16 (MN-major, 128B swizzle)
       ewait(s5done, ph);
       tc_fence_after();
+      if (et == 0) stamp(P, i, 5);  // D3 seen
       {
         uint8_t* b7 = base + kOffB7 + (i & 1) * G::kB7Bytes;
         uint32_t v[2][16];
@@ -679,6 +690,7 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       tc_fence_before();
       fence_proxy_async_smem();
       warp_arrive(e3, lane);
+      if (et == 0) stamp(P, i, 6);  // E3 done
       pX = X; pY = Y; pP = gi.u.p; pi = i; pstore = !gi.warm();
     }
     if (pi >= 0) do_e4(pi, pX, pY, pP, pstore);
