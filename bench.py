@@ -255,7 +255,9 @@ def run_b200(args):
     torch.cuda.synchronize()
     sus_clk = sus.stop()
     sus_ms = s0.elapsed_time(s1) / n_sus
-    launch_ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    launch_ms = sum(per_step) / K
+    median_ms = statistics.median(per_step)
     t = torch.tensor([total_ms, launch_ms], device=dev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -340,6 +342,7 @@ def run_b200(args):
             "steps": K,
             "warmup": args.warmup,
             "ms_per_step": round(ms_step, 5),
+            "ms_per_step_median": round(median_ms, 5),  # median of >= 20 steps
             "higher_is_better": True,
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None,
