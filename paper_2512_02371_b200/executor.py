@@ -622,7 +622,7 @@ def run_program_batch(p, inputs_list, extra_shapes=(), strict=False, lint_sink=N
         st = BufferStore()
         for n, data in host.items():
             k, loc = meta[n]
-            st[n] = Buffer(k, loc, data[t].copy())
+            st[n] = Buffer(k, loc, data[t])  # a view: each instance owns its row
         out.append(st)
     return out
 
@@ -645,11 +645,16 @@ def _run_group(lib, g, bufs, meta, T, dev, stream, err, scatter=None):
     import torch
     src, kern, acc = bufs[g.src], bufs[g.kern], bufs[g.acc]
     V = len(g.a_base)
-    keep = []
+    # the group's index tables are fixed per compiled plan: upload once per
+    # device and keep them on the group (plans are cached, _compiled)
+    cache = g.__dict__.setdefault("_dev_tables", {})
+    tables = cache.setdefault(str(dev), {})
 
-    def dptr(arr):
-        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32)).to(dev)
-        keep.append(t)
+    def dptr(arr, name):
+        t = tables.get(name)
+        if t is None:
+            t = tables[name] = torch.from_numpy(
+                np.ascontiguousarray(arr() if callable(arr) else arr, dtype=np.int32)).to(dev)
         return t.data_ptr()
 
     c = _lib.ConvGroup()
@@ -664,22 +669,25 @@ def _run_group(lib, g, bufs, meta, T, dev, stream, err, scatter=None):
     c.m, c.k, c.n, c.a_stride = g.m, g.k, g.n, g.a_stride
     c.iterations = V
     if g.a_idx:
-        comp = _compact(g.a_idx, g.b_idx) if V > 1 else None
+        if "compact" not in g.__dict__:
+            g.compact = _compact(g.a_idx, g.b_idx) if V > 1 else None
+        comp = g.compact
         if comp is not None:  # one gather table + a shift per iteration
-            c.a_idx, c.b_idx, c.a_shift = dptr(comp[0]), dptr(comp[1]), dptr(comp[2])
+            c.a_idx, c.b_idx = dptr(comp[0], "a_tab"), dptr(comp[1], "b_tab")
+            c.a_shift = dptr(comp[2], "a_shift")
         else:
-            c.a_idx = dptr(np.stack(g.a_idx))
-            c.b_idx = dptr(np.stack(g.b_idx))
+            c.a_idx = dptr(lambda: np.stack(g.a_idx), "a_idx")
+            c.b_idx = dptr(lambda: np.stack(g.b_idx), "b_idx")
     else:
-        c.a_base, c.k_base = dptr(g.a_base), dptr(g.k_base)
-        c.b_off = dptr(g.b_off)
+        c.a_base, c.k_base = dptr(g.a_base, "a_base"), dptr(g.k_base, "k_base")
+        c.b_off = dptr(g.b_off, "b_off")
     if scatter is not None:
         dst, bases, off = scatter
         out = bufs[dst]
         c.out, c.out_stride = out.data_ptr(), out.shape[1]
-        c.out_base = dptr(bases)
+        c.out_base = dptr(bases, "out_base")
         if off is not None:
-            c.out_off = dptr(off)
+            c.out_off = dptr(off, "out_off")
     err.zero_()
     c.error = err.data_ptr()
     _lib.check(lib.ts_run_conv_group(ctypes.byref(c), stream), "ts_run_conv_group")
