@@ -39,6 +39,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <mutex>
+#include <vector>
 
 #include "common.h"
 #include "sm100.cuh"
@@ -74,6 +76,11 @@ struct SepParams {
   int sb1, sb2;  // super-blocks per tile: 8 / m1 (pass 1), nb2 / m2 (pass 2)
   int R1;     // staged input rows per tile (multiple of 16)
   int nrt, nct, planes, ntiles;
+  // dynamic tile scheduling: CTAs claim tiles in order from *tile_next (and
+  // the last CTA to finish resets both counters for the next launch on the
+  // same stream); null = static round-robin
+  int* tile_next;
+  int* ctas_done;
   unsigned long long* trace;  // diagnostics: per-(CTA, tile, event) clock64 stamps or null
   int trace_ctas, trace_tiles;
   int ptab;      // 1: block tables below, 0: read r.tab / c.tab from global
@@ -129,32 +136,24 @@ __device__ __forceinline__ void store_out_row(uint32_t dst, uint32_t (&r)[16], c
 
 // Persistent tile walk t = blockIdx.x + it·gridDim.x with (p, rt, ct) kept
 // incrementally (one division at start, none per tile).
-struct TileWalk {
-  int t, ct, rt, p;
-  int dct, drt;
-  __device__ __forceinline__ explicit TileWalk(const SepParams& P) {
-    t = blockIdx.x;
-    ct = t % P.nct;
-    rt = (t / P.nct) % P.nrt;
-    p = t / (P.nct * P.nrt);
-    dct = gridDim.x % P.nct;
-    drt = gridDim.x / P.nct;
-  }
-  __device__ __forceinline__ void next(const SepParams& P) {
-    t += gridDim.x;
-    ct += dct;
-    int carry = 0;
-    if (ct >= P.nct) {
-      ct -= P.nct;
-      carry = 1;
-    }
-    rt += drt + carry;
-    while (rt >= P.nrt) {
-      rt -= P.nrt;
-      ++p;
-    }
-  }
+// Tiles in flight, by claim order: the producer writes the claimed tile of
+// iteration `it` to ring[it % kTileRing] before its stage's full barrier
+// completes; every later role reads it after its own wait (-1 = no more
+// tiles).  Claims run at most ~nst + 5 iterations ahead of the last role.
+constexpr int kTileRing = 16;
+
+struct TileXY {
+  int p, rt, ct;
 };
+
+__device__ __forceinline__ TileXY tile_xy(const SepParams& P, int t) {
+  TileXY r;
+  r.ct = t % P.nct;
+  const int rest = t / P.nct;
+  r.rt = rest % P.nrt;
+  r.p = rest / P.nrt;
+  return r;
+}
 
 template <typename OutT, int KQ1, int KQ2, bool EPI = false>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -177,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dh_free = dv_full + 9;
   uint64_t* wres = dv_full + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dv_full + 11);
+  volatile int* tile_ring = reinterpret_cast<volatile int*>(dv_full + 12);  // [kTileRing]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -223,10 +223,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_g2s(base + L.off_w + L.w1_bytes, P.c.tiles, cb, wres);
       }
       const int hr = P.R1 / 2;
-      TileWalk tw(P);
-      for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
+      for (int it = 0;; ++it) {
         const int s = it % nst;
         const uint32_t ph = (it / nst) & 1;
+        // claim the next tile: in order (dynamic) or round-robin (static)
+        int t = P.tile_next ? atomicAdd(P.tile_next, 1)
+                            : static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x);
+        if (t >= P.ntiles) t = -1;
+        trace_stamp(P, it, 0);
+        mbar_wait(&empty[s], ph ^ 1);
+        trace_stamp(P, it, 1);
+        tile_ring[it % kTileRing] = t;
+        if (t < 0) {  // no more tiles: complete the stage with no data
+          mbar_arrive(&full[s]);
+          break;
+        }
+        const TileXY tw = tile_xy(P, t);
         const int b1 = tw.rt * P.sb1, b2 = tw.ct * P.sb2;
         const int row0 = tab_ws(tab_r(P, b1)), col0 = tab_ws(tab_c(P, b2));
         uint32_t wbytes = 0;
@@ -238,9 +250,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j == 0 || tab_tid(tab_c(P, b2 + j)) != tab_tid(tab_c(P, b2 + j - 1)))
               wbytes += P.c.tile_bytes;
         }
-        trace_stamp(P, it, 0);
-        mbar_wait(&empty[s], ph ^ 1);
-        trace_stamp(P, it, 1);
         mbar_arrive_expect_tx(&full[s], L.in_stage + wbytes);
         uint8_t* dst = base + s * L.in_stage;
         tma_load_3d(dst, &tm_in, &full[s], col0, row0, tw.p);
@@ -273,16 +282,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tb1 = P.r.tile_bytes;
     const uint32_t sbo1 = static_cast<uint32_t>(P.r.K) * 16u;
     if (L.resident) mbar_wait(wres, 0);
-    TileWalk tw(P);
-    for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
+    for (int it = 0;; ++it) {
       const int s = it % nst;
       const int d = it & 1;
-      const int b1 = tw.rt * P.sb1;
-      const int row0 = tab_ws(tab_r(P, b1));
       const uint32_t a0 = base_s + s * L.in_stage;
       const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
       mbar_wait(&full[s], (it / nst) & 1);
       trace_stamp(P, it, 2);
+      const int t = tile_ring[it % kTileRing];
+      if (t < 0) {  // pass the end on to epilogue 1
+        mma_commit_elect(&dv_full[d]);
+        break;
+      }
+      const int b1 = tile_xy(P, t).rt * P.sb1;
+      const int row0 = tab_ws(tab_r(P, b1));
       mbar_wait(&dv_free[d], ((it >> 1) & 1) ^ 1);
       __syncwarp();
       tc_fence_after();
@@ -318,16 +331,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tb2 = P.c.tile_bytes;
     const uint32_t sbo2 = static_cast<uint32_t>(P.c.K) * 16u;
     if (L.resident) mbar_wait(wres, 0);
-    TileWalk tw(P);
-    for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
+    for (int it = 0;; ++it) {
       const int s = it % nst;
       const int m = it % nmid;
-      const int b2 = tw.ct * P.sb2;
-      const int col0 = tab_ws(tab_c(P, b2));
       const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
       const uint32_t mid_s = base_s + L.off_mid + m * kMidBytes;
       mbar_wait(&mid_full[m], (it / nmid) & 1);
       trace_stamp(P, it, 6);
+      const int t = tile_ring[it % kTileRing];
+      if (t < 0) {  // pass the end on to epilogue 2
+        mma_commit_elect(dh_full);
+        break;
+      }
+      const int b2 = tile_xy(P, t).ct * P.sb2;
+      const int col0 = tab_ws(tab_c(P, b2));
       mbar_wait(dh_free, (it & 1) ^ 1);
       __syncwarp();
       tc_fence_after();
@@ -361,14 +378,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;       // TMEM lane quarter this warp may access
     const int c = quarter * 32 + lane;  // input column within the tile
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    TileWalk tw(P);
-    for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
+    for (int it = 0;; ++it) {
       const int d = it & 1;
       const int m = it % nmid;
       const uint32_t mid_row =
           base_s + L.off_mid + m * kMidBytes + (c / 8) * 1024u + (c % 8) * 128u;
       mbar_wait(&dv_full[d], (it >> 1) & 1);
       if (warp == 2) trace_stamp(P, it, 4);
+      if (tile_ring[it % kTileRing] < 0) {  // pass the end on to the pass-2 issuer
+        mbar_arrive(&mid_full[m]);
+        break;
+      }
       mbar_wait(&mid_free[m], ((it / nmid) & 1) ^ 1);
       tc_fence_after();
 #pragma unroll
@@ -407,10 +427,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + 256u;
     const uint32_t out_row_bytes = static_cast<uint32_t>(nb2 * 16 * sizeof(OutT));
     const uint32_t orow = base_s + L.off_out + row * out_row_bytes;
-    TileWalk tw(P);
-    for (int it = 0; tw.t < P.ntiles; tw.next(P), ++it) {
+    for (int it = 0;; ++it) {
       mbar_wait(dh_full, it & 1);
       if (warp == 6) trace_stamp(P, it, 8);
+      const int t = tile_ring[it % kTileRing];
+      if (t < 0) break;
+      const TileXY tw = tile_xy(P, t);
       tc_fence_after();
       if (et == 0) bulk_wait_read0();  // previous TMA store finished reading staging
       named_bar_sync(2, 128);
@@ -447,6 +469,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
+  }
+  // the last CTA out resets the claim counters for the next launch on this
+  // stream (launches on one stream are ordered; streams get their own pair)
+  if (threadIdx.x == 0 && P.tile_next != nullptr) {
+    __threadfence();
+    if (atomicAdd(P.ctas_done, 1) == static_cast<int>(gridDim.x) - 1) {
+      atomicExch(P.tile_next, 0);
+      atomicExch(P.ctas_done, 0);
+      __threadfence();
+    }
   }
 }
 
@@ -602,6 +634,39 @@ static ts_status launch_sep(const SepParams& P, const CUtensorMap& tin, const CU
              : launch_sep_e<OutT, false>(P, tin, tout, stream);
 }
 
+// Tile-claim counters, one pair per (device, stream): launches on one stream
+// run in order, so a kernel's last CTA can reset its pair for the next one;
+// concurrent streams must not share a pair.
+static bool claim_counters(int device, cudaStream_t stream, int** next, int** done) {
+  constexpr int kSlots = 256;
+  struct Dev {
+    int* d = nullptr;
+    std::vector<cudaStream_t> streams;
+  };
+  static Dev devs[64];
+  static std::mutex mu;
+  if (device < 0 || device >= 64) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  Dev& D = devs[device];
+  if (!D.d) {
+    if (cudaMalloc(&D.d, 2 * kSlots * sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      D.d = nullptr;
+      return false;
+    }
+    if (cudaMemset(D.d, 0, 2 * kSlots * sizeof(int)) != cudaSuccess) return false;
+  }
+  size_t slot = 0;
+  while (slot < D.streams.size() && D.streams[slot] != stream) ++slot;
+  if (slot == D.streams.size()) {
+    if (slot >= static_cast<size_t>(kSlots)) return false;
+    D.streams.push_back(stream);
+  }
+  *next = D.d + 2 * slot;
+  *done = D.d + 2 * slot + 1;
+  return true;
+}
+
 static unsigned long long* g_trace = nullptr;
 static int g_trace_ctas = 0, g_trace_tiles = 0;
 
@@ -735,6 +800,10 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   }
   SepParams& P = hit->P;
   P.ep = make_epik(ep);
+  if (!claim_counters(ra->device, stream, &P.tile_next, &P.ctas_done)) {
+    P.tile_next = nullptr;  // out of counter slots: static round-robin tiles
+    P.ctas_done = nullptr;
+  }
   P.trace = g_trace;
   P.trace_ctas = g_trace_ctas;
   P.trace_tiles = g_trace_tiles;
