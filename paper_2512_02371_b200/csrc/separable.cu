@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -137,9 +138,10 @@ __device__ __forceinline__ void store_out_row(uint32_t dst, uint32_t (&r)[16], c
 // Persistent tile walk t = blockIdx.x + it·gridDim.x with (p, rt, ct) kept
 // incrementally (one division at start, none per tile).
 // Tiles in flight, by claim order: the producer writes the claimed tile of
-// iteration `it` to ring[it % kTileRing] before its stage's full barrier
-// completes; every later role reads it after its own wait (-1 = no more
-// tiles).  Claims run at most ~nst + 5 iterations ahead of the last role.
+// iteration `it` ({t, plane, row tile, column tile}) to ring slot
+// it % kTileRing before its stage's full barrier completes; every later role
+// reads it after its own wait (t = -1: no more tiles).  Claims run at most
+// ~nst + 5 iterations ahead of the last role.
 constexpr int kTileRing = 16;
 
 struct TileXY {
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dh_free = dv_full + 9;
   uint64_t* wres = dv_full + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dv_full + 11);
-  volatile int* tile_ring = reinterpret_cast<volatile int*>(dv_full + 12);  // [kTileRing]
+  volatile int* tile_ring = reinterpret_cast<volatile int*>(dv_full + 12);  // [kTileRing][4]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -223,21 +225,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_g2s(base + L.off_w + L.w1_bytes, P.c.tiles, cb, wres);
       }
       const int hr = P.R1 / 2;
+      // claim tiles in order (dynamic) or round-robin (static); the claim for
+      // the next iteration is issued one iteration early so the atomic's
+      // round trip overlaps this tile's stage wait and TMA issue
+      auto claim = [&](int it) {
+        return P.tile_next ? atomicAdd(P.tile_next, 1)
+                           : static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x);
+      };
+      int t_next = claim(0);
       for (int it = 0;; ++it) {
         const int s = it % nst;
         const uint32_t ph = (it / nst) & 1;
-        // claim the next tile: in order (dynamic) or round-robin (static)
-        int t = P.tile_next ? atomicAdd(P.tile_next, 1)
-                            : static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x);
+        int t = t_next;
         if (t >= P.ntiles) t = -1;
-        trace_stamp(P, it, 0);
-        mbar_wait(&empty[s], ph ^ 1);
-        trace_stamp(P, it, 1);
-        tile_ring[it % kTileRing] = t;
-        if (t < 0) {  // no more tiles: complete the stage with no data
+        if (t < 0) {  // no more tiles: complete a stage with no data
+          mbar_wait(&empty[s], ph ^ 1);
+          tile_ring[4 * (it % kTileRing)] = -1;
           mbar_arrive(&full[s]);
           break;
         }
+        t_next = claim(it + 1);
+        // everything about the tile is computed before the stage wait, so
+        // the TMA issue follows the wait immediately (the ring period sets
+        // the kernel's pace)
         const TileXY tw = tile_xy(P, t);
         const int b1 = tw.rt * P.sb1, b2 = tw.ct * P.sb2;
         const int row0 = tab_ws(tab_r(P, b1)), col0 = tab_ws(tab_c(P, b2));
@@ -250,6 +260,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j == 0 || tab_tid(tab_c(P, b2 + j)) != tab_tid(tab_c(P, b2 + j - 1)))
               wbytes += P.c.tile_bytes;
         }
+        trace_stamp(P, it, 0);
+        mbar_wait(&empty[s], ph ^ 1);
+        trace_stamp(P, it, 1);
+        volatile int* tslot = tile_ring + 4 * (it % kTileRing);
+        tslot[0] = t;
+        tslot[1] = tw.p;
+        tslot[2] = tw.rt;
+        tslot[3] = tw.ct;
         mbar_arrive_expect_tx(&full[s], L.in_stage + wbytes);
         uint8_t* dst = base + s * L.in_stage;
         tma_load_3d(dst, &tm_in, &full[s], col0, row0, tw.p);
@@ -289,12 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t w0 = L.resident ? base_s + L.off_w : base_s + L.off_w + s * L.w_stage;
       mbar_wait(&full[s], (it / nst) & 1);
       trace_stamp(P, it, 2);
-      const int t = tile_ring[it % kTileRing];
-      if (t < 0) {  // pass the end on to epilogue 1
+      const volatile int* tslot = tile_ring + 4 * (it % kTileRing);
+      if (tslot[0] < 0) {  // pass the end on to epilogue 1
         mma_commit_elect(&dv_full[d]);
         break;
       }
-      const int b1 = tile_xy(P, t).rt * P.sb1;
+      const int b1 = tslot[2] * P.sb1;
       const int row0 = tab_ws(tab_r(P, b1));
       mbar_wait(&dv_free[d], ((it >> 1) & 1) ^ 1);
       __syncwarp();
@@ -338,12 +356,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t mid_s = base_s + L.off_mid + m * kMidBytes;
       mbar_wait(&mid_full[m], (it / nmid) & 1);
       trace_stamp(P, it, 6);
-      const int t = tile_ring[it % kTileRing];
-      if (t < 0) {  // pass the end on to epilogue 2
+      const volatile int* tslot = tile_ring + 4 * (it % kTileRing);
+      if (tslot[0] < 0) {  // pass the end on to epilogue 2
         mma_commit_elect(dh_full);
         break;
       }
-      const int b2 = tile_xy(P, t).ct * P.sb2;
+      const int b2 = tslot[3] * P.sb2;
       const int col0 = tab_ws(tab_c(P, b2));
       mbar_wait(dh_free, (it & 1) ^ 1);
       __syncwarp();
@@ -385,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           base_s + L.off_mid + m * kMidBytes + (c / 8) * 1024u + (c % 8) * 128u;
       mbar_wait(&dv_full[d], (it >> 1) & 1);
       if (warp == 2) trace_stamp(P, it, 4);
-      if (tile_ring[it % kTileRing] < 0) {  // pass the end on to the pass-2 issuer
+      if (tile_ring[4 * (it % kTileRing)] < 0) {  // pass the end on to the pass-2 issuer
         mbar_arrive(&mid_full[m]);
         break;
       }
@@ -430,9 +448,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0;; ++it) {
       mbar_wait(dh_full, it & 1);
       if (warp == 6) trace_stamp(P, it, 8);
-      const int t = tile_ring[it % kTileRing];
-      if (t < 0) break;
-      const TileXY tw = tile_xy(P, t);
+      const volatile int* tslot = tile_ring + 4 * (it % kTileRing);
+      if (tslot[0] < 0) break;
+      TileXY tw;
+      tw.p = tslot[1];
+      tw.rt = tslot[2];
+      tw.ct = tslot[3];
       tc_fence_after();
       if (et == 0) bulk_wait_read0();  // previous TMA store finished reading staging
       named_bar_sync(2, 128);
@@ -547,7 +568,7 @@ static bool plan_smem(SepParams& P, int oes) {
   const uint32_t st_w1 = static_cast<uint32_t>(P.sb1) * tb1;
   const uint32_t st_bytes = align_up(st_w1 + static_cast<uint32_t>(P.sb2) * tb2, 1024);
   const uint32_t out_bytes = align_up(128u * P.nb2 * 16u * oes, 1024);
-  const uint32_t fixed = out_bytes + 256 + 1024;  // barriers + alignment slack
+  const uint32_t fixed = out_bytes + 512 + 1024;  // barriers + tile ring + alignment slack
   // (a single input stage was measured slower than two axis passes: 2048^2 ->
   // 921^2 at 48 planes 0.280 vs 0.248 ms, so plans need >= 2 stages)
   for (uint32_t nmid = 2; nmid >= 1; --nmid) {
@@ -567,7 +588,7 @@ static bool plan_smem(SepParams& P, int oes) {
         L.off_mid = L.off_w + wb;
         L.off_out = L.off_mid + nmid * kMidBytes;
         L.off_bar = L.off_out + out_bytes;
-        L.total = L.off_bar + 256 + 1024;
+        L.total = L.off_bar + 512 + 1024;
         return true;
       }
     }
@@ -800,8 +821,21 @@ ts_status separable_run(const ts_axis* ra, const ts_axis* ca, int planes, const 
   }
   SepParams& P = hit->P;
   P.ep = make_epik(ep);
-  if (!claim_counters(ra->device, stream, &P.tile_next, &P.ctas_done)) {
-    P.tile_next = nullptr;  // out of counter slots: static round-robin tiles
+  // Tile order.  Static round-robin (CTA b takes tiles b, b + grid, ...)
+  // keeps the ~grid tiles in flight contiguous, so neighbouring tiles share
+  // their halo rows / columns in L2 — until the CTAs drift apart: beyond
+  // ~128 tiles per CTA the in-flight set spreads, halos are evicted and DRAM
+  // reads grow (48 frames of c2 in one launch: 1.68x algorithmic).  Long
+  // launches therefore claim tiles in order from a counter (DRAM 1.00x at
+  // any length); short ones keep the counter-free static order, which is a
+  // few per cent faster there (c2, 16 frames: 0.848 vs 0.82 of HBM).
+  // TSB_STATIC_TILES=1 / TSB_DYNAMIC_TILES=1 force either.
+  static const bool force_static = std::getenv("TSB_STATIC_TILES") != nullptr;
+  static const bool force_dynamic = std::getenv("TSB_DYNAMIC_TILES") != nullptr;
+  const bool dynamic = !force_static &&
+                       (force_dynamic || P.ntiles > 128 * sm_count_current());
+  if (!dynamic || !claim_counters(ra->device, stream, &P.tile_next, &P.ctas_done)) {
+    P.tile_next = nullptr;  // static round-robin tiles
     P.ctas_done = nullptr;
   }
   P.trace = g_trace;
