@@ -115,3 +115,19 @@ def test_pipelines_refuse_host_arrays():
     from paper_2512_02371_b200 import pipelines
     with pytest.raises(errors.NoDevice):
         pipelines.resample(np.zeros((4, 4), np.float32), 2, 2)
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: without the native library every product entry point
+    raises NativeLibraryMissing (here: the binding pointed at a missing file)."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, torch\n"
+            "from paper_2512_02371_b200 import _lib, axis, executor, pipelines\n"
+            "try:\n    _lib.load()\nexcept _lib.NativeLibraryMissing:\n    pass\n"
+            "else:\n    raise SystemExit('load() succeeded')\n"
+            "try:\n    axis.lanczos3(64, 32, 0)\nexcept _lib.NativeLibraryMissing:\n    print('ok')\n")
+    env = {**os.environ, "TSB_LIB_PATH": "/nonexistent/libtsb200.so", "PYTHONPATH": ROOT}
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=ROOT)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
