@@ -112,7 +112,16 @@ class ClockSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            h = None
+            try:  # NVML numbers GPUs ignoring CUDA_VISIBLE_DEVICES: match by PCI bus id
+                import torch
+                pr = torch.cuda.get_device_properties(self.gpu)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception as e:  # no NVML: report why instead of inventing clocks
             self.err = f"nvml unavailable: {e}"
@@ -171,9 +180,9 @@ def run_b200(args):
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
+    torch.cuda.set_device(local)  # before the NCCL group: each rank on its own GPU
     if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     H, W, oh, ow, op, taps, desc = CONFIGS[args.config]
     F = args.frames
