@@ -99,3 +99,39 @@ def test_two_gloo_ranks_on_one_gpu_bitwise():
         p.join(timeout=300)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5) is True
+
+
+def test_dynamic_tile_claiming_over_concurrent_streams():
+    """In-order tile claiming (the fused kernel's long-launch mode, forced
+    here for short launches with TSB_DYNAMIC_TILES=1) keeps one counter pair
+    per stream: run_from_host's three concurrent streams and a large single
+    launch must reproduce the static-order result bit for bit."""
+    import subprocess
+    import sys
+    code = r"""
+import os, sys, torch
+from paper_2512_02371_b200 import pipelines
+g = torch.Generator(device="cpu").manual_seed(9)
+x = torch.rand((36, 540, 960), generator=g).bfloat16()
+want = torch.load(sys.argv[1])
+one = pipelines.downsample2x(x.cuda()).cpu()
+host_out = torch.empty_like(one).pin_memory()
+for _ in range(3):
+    pipelines.run_from_host(pipelines.downsample2x, x.pin_memory(), host_out, chunk_planes=3)
+    torch.cuda.synchronize()
+    assert torch.equal(host_out.view(torch.int16), want.view(torch.int16))
+assert torch.equal(one.view(torch.int16), want.view(torch.int16))
+print("ok")
+"""
+    import tempfile
+    import torch
+    from paper_2512_02371_b200 import pipelines
+    g = torch.Generator(device="cpu").manual_seed(9)
+    x = torch.rand((36, 540, 960), generator=g).bfloat16()
+    want = pipelines.downsample2x(x.cuda()).cpu()  # this process: static order
+    with tempfile.NamedTemporaryFile(suffix=".pt") as f:
+        torch.save(want, f.name)
+        env = {**os.environ, "TSB_DYNAMIC_TILES": "1"}
+        r = subprocess.run([sys.executable, "-c", code, f.name], capture_output=True, text=True,
+                           env=env, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
