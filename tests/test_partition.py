@@ -1,6 +1,8 @@
-"""Partitioner: pure index arithmetic — covered on CPU, including
-a 2-process gloo run that shards one image into row bands and frames across
-ranks and checks the gathered result against the single-process oracle."""
+"""Partitioner index arithmetic on CPU: frame shards, row bands
+with read-only halos, band-local axes and composed axes, checked by
+evaluating them with the oracle — including a 2-process gloo run of that
+index math.  The same paths on the real kernels (frame shards, row bands,
+two ranks on one GPU) are tests/test_gpu_multi.py."""
 
 import os
 import socket
@@ -94,7 +96,9 @@ def _worker(rank, ws, port, q):
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_sharding():
+def test_two_rank_gloo_index_math():
+    """Index math only: each rank evaluates its row band / frame shard with
+    the oracle; the gathered bands equal the full-image oracle."""
     import torch.multiprocessing as mp
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
