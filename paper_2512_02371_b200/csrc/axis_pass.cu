@@ -1,27 +1,40 @@
-// axis_pass.cu — one banded axis applied along rows or columns of planar
-// images, for geometries the fused separable kernel cannot tile (windows of
-// more than ~128-512 inputs per 16 outputs: large downscale factors, very
-// wide filters).  A resample then runs as two passes with a
-// bf16 intermediate in HBM (the same rounding point as the fused kernel's V):
+// axis_pass.cu — one banded axis applied along rows ("vertical") or columns
+// ("horizontal") of planar images, for geometries the fused separable kernel
+// cannot tile (windows of more than ~128-512 inputs per 16 outputs: large
+// downscale factors, very wide filters).  A resample then
+// runs as two passes with a bf16 intermediate in HBM (the same rounding
+// point as the fused kernel's V):
 //
 //   vertical   mid[p][o][c] = Σ_k R[o][k] in[p][k][c]
-//              A = 16 input rows x 128 columns per K-step (TMA, MN-major,
-//              128B swizzle), B = the block's K x 16 weight tile,
-//              D (TMEM) lane = column, 16 outputs
+//              A = 64 input rows x 128 columns per ring slot (two 64-column
+//              TMA boxes, MN-major, 128B swizzle) = 4 K-steps of 16 rows,
+//              B = the block's K x 16 weight tile, D (TMEM) lane = column
 //   horizontal out[p][r][j] = Σ_k mid[p][r][k] C[j][k]
-//              A = 128 rows x 16 columns per K-step (TMA, K-major core
-//              matrices), B = the block's weight tile, D lane = row
+//              A = 128 rows x 64 columns per ring slot (one K-major 128B
+//              swizzled box) = 4 K-steps of 16 columns, D lane = row
 //
-// One CTA per (plane, group of up to 8 16-output blocks, 128-wide strip);
-// each block's K window streams through an 8-slot TMA ring with no upper
-// bound on its length (windows up to 1024 inputs, i.e. ~45x downscale), the
-// blocks accumulate into adjacent 16-column TMEM slices and leave in one TMA
-// store.  Several CTAs share an SM (the ring depth, group size and TMEM
-// columns are sized per pass so that loads from many CTAs overlap).
+// A unit = (plane, group of nbg 16-output blocks, 128-wide strip); each
+// block's K window (up to 1024 inputs, ~45x downscale) streams through the
+// ring, the group's blocks accumulate into adjacent 16-column TMEM slices
+// and leave in one TMA store.
+//
+// Persistent CTAs: a kernel that contains tcgen05 (TMEM) instructions starts
+// CTAs ~4x slower than a plain kernel (tools/probes/launch_rate.cu on B200:
+// ~250 vs ~1000 CTAs/us for the whole GPU), so one short-lived CTA per unit
+// made these passes launch-rate bound (22k CTAs >= 89 us of the vertical
+// pass's 131 us at 2048^2 -> 921^2, 48 planes).  Each CTA here keeps its
+// barriers and TMEM and takes units strided over the grid:
+//
+//   warp 0     producer: the unit's weight tiles (bulk copy) into one of two
+//              weight buffers, then every block's K window through the ring
+//   warp 1     MMA issuer: N = 16 per block into one of two TMEM
+//              accumulators, so unit k+1 accumulates while unit k drains
+//   warps 2-5  epilogue: TMEM -> registers -> staging -> one TMA store
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -30,73 +43,81 @@
 
 namespace tsb {
 
+int sm_count_current();
 ts_status encode_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* ptr,
                          int64_t d0, int64_t d1, int64_t d2, int64_t stride1_elems,
                          int64_t stride2_elems, int box0, int box1, CUtensorMapSwizzle swz);
 
 namespace apass {
 
-constexpr int kThreads = 128;
-// ring slot: vertical = one K-step (16 rows x 128 columns, two 64-column
-// boxes); horizontal = four K-steps (128 rows x 64 columns, one 128B-swizzled
-// K-major box: 128-byte rows keep the TMA efficient)
-template <bool VERT>
-struct Ring {
-  static constexpr int kSlots = VERT ? 6 : 4;
-  static constexpr uint32_t kSlot = VERT ? 4096u : 16384u;
-  static constexpr int kSteps = VERT ? 1 : 4;  // K-steps per slot
+constexpr int kThreads = 192;
+constexpr uint32_t kSlot = 16384;  // 4 K-steps of A
+constexpr int kMaxRing = 4;
+
+// a decoded unit, handed from the producer to the MMA and epilogue warps
+struct Unit {
+  int live;  // 0 = end of work
+  int p, b0, nblk, strip;
 };
 
 struct Params {
   AxisDev ax;
-  int planes, nb, nstrip;  // blocks along the axis, 128-wide strips across it
-  int nbg, ngroups;        // blocks per CTA (<= 8) and block groups
+  int nb, nstrip, nbg, ngroups;
+  int nq;      // K-steps per block (K / 16)
+  int nchunk;  // ring slots per block
   int nunits;
-  uint32_t tmem_cols;  // accumulator columns: 16 per block, power of two >= 32
-  int nring;  // ring slots in use (<= Ring::kSlots): a group never needs more than it loads
-  uint32_t off_b, off_out, off_bar;
+  int nring;        // ring slots in use
+  uint32_t tcols;   // TMEM columns per accumulator buffer
+  uint32_t wbytes;  // bytes per weight buffer
+  uint32_t off_w, off_out, off_bar;
   EpiK ep;  // output epilogue (EPI kernels only)
 };
 
+__device__ __forceinline__ void write_unit(Unit* dst, const Unit& u) {
+  volatile int* d = reinterpret_cast<volatile int*>(dst);
+  d[0] = u.live, d[1] = u.p, d[2] = u.b0, d[3] = u.nblk, d[4] = u.strip;
+}
+
+__device__ __forceinline__ Unit read_unit(const Unit* src) {
+  const volatile int* s = reinterpret_cast<const volatile int*>(src);
+  Unit u;
+  u.live = s[0], u.p = s[1], u.b0 = s[2], u.nblk = s[3], u.strip = s[4];
+  return u;
+}
+
+// (at most 4 CTAs per SM fit the shared-memory layouts: 85 registers each)
 template <bool VERT, typename OutT, bool EPI>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
     axis_pass_kernel(const __grid_constant__ CUtensorMap tm_in,
                      const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ Params P) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_s = smem_u32(smem_raw);
   const uint32_t base_s = (raw_s + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_s - raw_s);
-  const uint32_t tile_bytes = static_cast<uint32_t>(P.ax.tile_bytes);
-  // [ring][B tiles of the group][staging][barriers]
-  using RG = Ring<VERT>;
-  constexpr int kRing = RG::kSlots;  // barrier array size
-  const int nring = P.nring;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + P.off_bar);
   uint64_t* full = bars;
-  uint64_t* empty = bars + kRing;
-  uint64_t* wbar = bars + 2 * kRing;
-  uint64_t* done = wbar + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* empty = bars + kMaxRing;
+  uint64_t* wfull = bars + 2 * kMaxRing;  // [2] weights + unit info landed
+  uint64_t* ufree = wfull + 2;            // [2] epilogue done with buffer b (4 arrivals)
+  uint64_t* afull = ufree + 2;            // [2] accumulator b complete
+  Unit* units = reinterpret_cast<Unit*>(afull + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(units + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  const int u = blockIdx.x;
-  const int strip = u % P.nstrip;
-  const int g = (u / P.nstrip) % P.ngroups;
-  const int p = u / (P.nstrip * P.ngroups);
-  const int b0 = g * P.nbg;
-  const int nblk = min(P.nbg, P.nb - b0);
-  const int nq = P.ax.K / 16;
+  const uint32_t tb = static_cast<uint32_t>(P.ax.tile_bytes);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRing; ++s) {
+    for (int s = 0; s < kMaxRing; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(wbar, 1);
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&wfull[b], 1);
+      mbar_init(&ufree[b], 4);
+      mbar_init(&afull[b], 1);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc_n(tmem_slot, P.tmem_cols);
+  if (warp == 1) tmem_alloc_n(tmem_slot, 2 * P.tcols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -104,143 +125,193 @@ __global__ void __launch_bounds__(kThreads)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(wbar, tile_bytes * nblk);
-      for (int j = 0; j < nblk; ++j) {
-        const int tid = __ldg(P.ax.tid + b0 + j);
-        bulk_g2s(base + P.off_b + j * tile_bytes, P.ax.tiles + static_cast<size_t>(tid) * tile_bytes,
-                 tile_bytes, wbar);
-      }
       int s = 0;
       uint32_t ph = 0;
-      const int nslot = (nq + RG::kSteps - 1) / RG::kSteps;
-      for (int j = 0; j < nblk; ++j) {
-        const int ws = __ldg(P.ax.ws + b0 + j);  // window start (may be negative)
-        for (int q = 0; q < nslot; ++q) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], RG::kSlot);
-          uint8_t* dst = base + s * RG::kSlot;
-          if (VERT) {  // rows ws+16q.., columns 128*strip.. as two 64-column boxes
-            tma_load_3d(dst, &tm_in, &full[s], 128 * strip, ws + 16 * q, p);
-            tma_load_3d(dst + 2048, &tm_in, &full[s], 128 * strip + 64, ws + 16 * q, p);
-          } else {     // rows 128*strip.., columns ws+64q.. as one 64-column box
-            tma_load_3d(dst, &tm_in, &full[s], ws + 64 * q, 128 * strip, p);
-          }
-          if (++s == nring) {
-            s = 0;
-            ph ^= 1;
+      for (int k = 0;; ++k) {
+        const int u = blockIdx.x + k * gridDim.x;
+        const int b = k & 1;
+        // buffer b (unit info, weights) was last used by unit k - 2
+        if (k >= 2) mbar_wait(&ufree[b], ((k >> 1) - 1) & 1);
+        Unit U{};
+        if (u >= P.nunits) {
+          write_unit(&units[b], U);
+          mbar_arrive(&wfull[b]);
+          break;
+        }
+        const int local = u % (P.nstrip * P.ngroups);
+        U.live = 1;
+        U.p = u / (P.nstrip * P.ngroups);
+        U.strip = local % P.nstrip;
+        U.b0 = (local / P.nstrip) * P.nbg;
+        U.nblk = min(P.nbg, P.nb - U.b0);
+        write_unit(&units[b], U);
+        mbar_arrive_expect_tx(&wfull[b], tb * U.nblk);
+        uint8_t* wb = base + P.off_w + b * P.wbytes;
+        for (int j = 0; j < U.nblk; ++j) {
+          const int tid = __ldg(P.ax.tid + U.b0 + j);
+          bulk_g2s(wb + j * tb, P.ax.tiles + static_cast<size_t>(tid) * tb, tb, &wfull[b]);
+        }
+        for (int j = 0; j < U.nblk; ++j) {
+          const int ws = __ldg(P.ax.ws + U.b0 + j);  // window start (may be negative)
+          for (int c = 0; c < P.nchunk; ++c) {
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&full[s], kSlot);
+            uint8_t* dst = base + s * kSlot;
+            if (VERT) {  // rows ws+64c.., columns 128*strip.. as two 64-column boxes
+              tma_load_3d(dst, &tm_in, &full[s], 128 * U.strip, ws + 64 * c, U.p);
+              tma_load_3d(dst + kSlot / 2, &tm_in, &full[s], 128 * U.strip + 64, ws + 64 * c, U.p);
+            } else {  // rows 128*strip.., columns ws+64c..
+              tma_load_3d(dst, &tm_in, &full[s], ws + 64 * c, 128 * U.strip, U.p);
+            }
+            if (++s == P.nring) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc = make_idesc(kFmtBF16, 128, 16, VERT ? 1u : 0u, 0u);
-    const uint64_t bd0 = make_sdesc(base_s + P.off_b, 128u, static_cast<uint32_t>(P.ax.K) * 16u,
-                                    kSwizzleNone);
-    // vertical: MN-major SW128 (64-column atoms 2 KB apart, 8-row groups at
-    // 1 KB); horizontal: K-major SW128 (8-row groups at 1 KB, K-steps are
-    // 32-byte advances inside the swizzle atom)
-    const uint64_t ad0 = VERT ? make_sdesc(base_s, 2048u, 1024u, kSwizzle128B)
-                              : make_sdesc(base_s, 16u, 1024u, kSwizzle128B);
-    mbar_wait(wbar, 0);
     int s = 0;
     uint32_t ph = 0;
-    for (int j = 0; j < nblk; ++j) {
-      const uint64_t bdj = bd0 + static_cast<uint64_t>(j * (tile_bytes >> 4));
-      for (int q0 = 0; q0 < nq; q0 += RG::kSteps) {
-        mbar_wait(&full[s], ph);
-        __syncwarp();
-        tc_fence_after();
-        const uint64_t ads = ad0 + static_cast<uint64_t>(s * (RG::kSlot >> 4));
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      const uint32_t n = static_cast<uint32_t>(k >> 1);
+      mbar_wait(&wfull[b], n & 1);
+      const Unit U = read_unit(&units[b]);
+      if (!U.live) break;
+      if (k >= 2) mbar_wait(&ufree[b], (n - 1) & 1);  // accumulator b drained
+      tc_fence_after();
+      const uint64_t bd0 = make_sdesc(base_s + P.off_w + b * P.wbytes, 128u,
+                                      static_cast<uint32_t>(P.ax.K) * 16u, kSwizzleNone);
+      const uint32_t acc = tmem + b * P.tcols;
+      for (int j = 0; j < U.nblk; ++j) {
+        const uint64_t bdj = bd0 + static_cast<uint64_t>(j * (tb >> 4));
+        for (int c = 0; c < P.nchunk; ++c) {
+          mbar_wait(&full[s], ph);
+          __syncwarp();
+          tc_fence_after();
+          const uint32_t sa = base_s + s * kSlot;
+          // vertical: MN-major SW128, the two 64-column halves 8 KB apart,
+          // K-steps of 16 rows 2 KB apart; horizontal: K-major SW128, K-steps
+          // 32 bytes apart inside the swizzle atom
+          const uint64_t ad = VERT ? make_sdesc(sa, kSlot / 2, 1024u, kSwizzle128B)
+                                   : make_sdesc(sa, 16u, 1024u, kSwizzle128B);
+          constexpr uint32_t adv = VERT ? 2048u >> 4 : 32u >> 4;
 #pragma unroll
-        for (int u = 0; u < RG::kSteps; ++u) {
-          const int q = q0 + u;
-          if (q < nq)
-            mma_f16_ss_elect(tmem + 16u * j, ads + static_cast<uint64_t>(u * 2), bdj + 16u * q,
-                             idesc, q > 0 ? 1u : 0u);
-        }
-        mma_commit_elect(&empty[s]);
-        if (++s == nring) {
-          s = 0;
-          ph ^= 1;
+          for (int i = 0; i < 4; ++i) {
+            const int q = 4 * c + i;
+            if (q < P.nq)
+              mma_f16_ss_elect(acc + 16u * j, ad + static_cast<uint64_t>(i * adv), bdj + 16u * q,
+                               idesc, q > 0 ? 1u : 0u);
+          }
+          mma_commit_elect(&empty[s]);
+          if (++s == P.nring) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
+      mma_commit_elect(&afull[b]);
     }
-    mma_commit_elect(done);
-  }
-  // epilogue: all four warps (lane = TMEM row)
-  mbar_wait(done, 0);
-  __syncwarp();  // reconverge warp 0 (lane 0 ran the producer loop)
-  tc_fence_after();
-  const int row = warp * 32 + lane;
-  const uint32_t tl = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  OutT* stg = reinterpret_cast<OutT*>(base + P.off_out);
-#pragma unroll 1
-  for (int j = 0; j < nblk; ++j) {
-    uint32_t r[16];
-    tmem_ld16(tl + 16u * j, r);
-    tmem_wait_ld();
-    if constexpr (EPI) {
+  } else {
+    // epilogue warps 2-5: TMEM lane quadrant = warp % 4
+    const int et = threadIdx.x - 64;
+    const int qd = warp & 3;
+    const int row = qd * 32 + lane;
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      const uint32_t n = static_cast<uint32_t>(k >> 1);
+      mbar_wait(&wfull[b], n & 1);
+      const Unit U = read_unit(&units[b]);
+      if (!U.live) break;
+      mbar_wait(&afull[b], n & 1);
+      tc_fence_after();
+      named_bar_sync(1, 128);  // staging free: the previous store has read it
+      const uint32_t tl = tmem + (static_cast<uint32_t>(qd * 32) << 16) + b * P.tcols;
+      OutT* stg = reinterpret_cast<OutT*>(base + P.off_out);
+      for (int j = 0; j < U.nblk; ++j) {
+        uint32_t r[16];
+        tmem_ld16(tl + 16u * j, r);
+        tmem_wait_ld();
+        if constexpr (EPI) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(epi_f32(P.ep, __uint_as_float(r[i])));
-    }
-    if (VERT) {  // lane = column c, values = 16 output rows: staging [nout][128]
+          for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(epi_f32(P.ep, __uint_as_float(r[i])));
+        }
+        if (VERT) {  // lane = column, values = 16 output rows: staging [16 nbg][128]
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float v = __uint_as_float(r[i]);
-        if constexpr (sizeof(OutT) == 2)
-          stg[(16 * j + i) * 128 + row] = __float2bfloat16_rn(v);
+          for (int i = 0; i < 16; ++i) {
+            const float v = __uint_as_float(r[i]);
+            if constexpr (sizeof(OutT) == 2)
+              stg[(16 * j + i) * 128 + row] = __float2bfloat16_rn(v);
+            else
+              stg[(16 * j + i) * 128 + row] = v;
+          }
+        } else {  // lane = row, values = 16 output columns: staging [128][16 nbg]
+          OutT* d = stg + row * (16 * P.nbg) + 16 * j;
+          if constexpr (sizeof(OutT) == 2) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+            uint4* d4 = reinterpret_cast<uint4*>(d);
+            d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          } else {
+            uint4* d4 = reinterpret_cast<uint4*>(d);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              d4[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ufree[b]);  // accumulator, weights and unit info free
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (et == 0) {
+        // the box covers nbg blocks; a short last group is clipped by the axis end
+        if (VERT)
+          tma_store_3d(&tm_out, stg, 128 * U.strip, 16 * U.b0, U.p);
         else
-          stg[(16 * j + i) * 128 + row] = v;
-      }
-    } else {     // lane = row r, values = 16 output columns: staging [128][nout]
-      OutT* d = stg + row * (16 * P.nbg) + 16 * j;  // box row pitch: nbg blocks
-      if constexpr (sizeof(OutT) == 2) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-        uint4* d4 = reinterpret_cast<uint4*>(d);
-        d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      } else {
-        uint4* d4 = reinterpret_cast<uint4*>(d);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          d4[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+          tma_store_3d(&tm_out, stg, 16 * U.b0, 128 * U.strip, U.p);
+        bulk_commit();
+        bulk_wait_read0();  // staging may be rewritten once read; the write completes on its own
       }
     }
   }
-  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // the box covers nbg blocks; a short last group is clipped by the axis end
-    if (VERT)
-      tma_store_3d(&tm_out, stg, 128 * strip, 16 * b0, p);
-    else
-      tma_store_3d(&tm_out, stg, 16 * b0, 128 * strip, p);
-    bulk_commit();
-    bulk_wait_read0();  // smem may be released once read; the write completes on its own
-  }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc_n(tmem, P.tmem_cols);
+    tmem_dealloc_n(tmem, 2 * P.tcols);
   }
 }
 
-template <bool VERT, typename OutT>
+template <bool VERT, typename OutT, bool EPI>
 static cudaError_t launch(const Params& P, const CUtensorMap& tin, const CUtensorMap& tout,
-                          uint32_t smem, cudaStream_t stream, bool epi) {
-  if (epi) {
-    auto k = axis_pass_kernel<VERT, OutT, true>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) k<<<P.nunits, kThreads, smem, stream>>>(tin, tout, P);
-    return e;
+                          int grid, uint32_t smem, cudaStream_t stream) {
+  auto k = axis_pass_kernel<VERT, OutT, EPI>;
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr_done[dev] = true;
   }
-  auto k = axis_pass_kernel<VERT, OutT, false>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) k<<<P.nunits, kThreads, smem, stream>>>(tin, tout, P);
-  return e;
+  k<<<grid, kThreads, smem, stream>>>(tin, tout, P);
+  return cudaGetLastError();
+}
+
+template <bool VERT, bool EPI>
+static cudaError_t launch_t(int out_dtype, const Params& P, const CUtensorMap& tin,
+                            const CUtensorMap& tout, int grid, uint32_t smem,
+                            cudaStream_t stream) {
+  return out_dtype == TS_BF16 ? launch<VERT, __nv_bfloat16, EPI>(P, tin, tout, grid, smem, stream)
+                              : launch<VERT, float, EPI>(P, tin, tout, grid, smem, stream);
 }
 
 }  // namespace apass
@@ -266,58 +337,57 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
     return set_error(TS_ERR_INVALID, "axis_pass: strides");
   DeviceGuard guard(a->device);
   if (guard.err != cudaSuccess) return cuda_error(guard.err, "cudaSetDevice");
-  apass::Params P;
+
+  apass::Params P{};
   P.ep = make_epik(ep);
   P.ax = a->dev();
-  P.planes = planes;
   P.nb = a->nb;
   P.nstrip = ((dim == 0 ? W : H) + 127) / 128;
-  // blocks per CTA: more blocks amortise the per-CTA setup, fewer keep more
-  // CTAs (and so more 2 KB TMA boxes) in flight per SM, which is what the
-  // load path needs — group only when there are plenty of units
+  P.nq = a->K / 16;
+  P.nchunk = (P.nq + 3) / 4;
+  // wide windows (K >= 128: each block already streams >= 2 slots) run one
+  // block per unit through a 3-slot ring; narrower ones two blocks per unit
+  // (the weight copy and the store amortised) through 2 slots — measured on
+  // B200 over nbg 1/2/4 x ring 1-4, 2048^2 -> {921, 450, 245, 143}^2 and
+  // 4K -> 540p, 48 planes (K4)
+  const bool wide = a->K >= 128;
+  P.nbg = wide ? 1 : 2;
+  P.nring = wide ? 3 : 2;
+  if (const char* f = std::getenv("TSB_APASS_NBG")) P.nbg = std::max(1, std::atoi(f));
+  if (const char* f = std::getenv("TSB_APASS_RING")) P.nring = std::atoi(f);
+  P.nbg = std::min(std::min(P.nbg, 8), P.nb);
+  P.nring = std::max(1, std::min(P.nring, apass::kMaxRing));
   const uint32_t tb = static_cast<uint32_t>(a->tile_bytes);
-  const int64_t base_units = static_cast<int64_t>(planes) * a->nb * P.nstrip;
-  P.nbg = 1;
-  // (measured on B200, tools/sweep_apass.sh: 4K->540p and 2048^2->{143,450,921}^2)
-  if (dim == 0) {
-    const int64_t want = 148 * 64;
-    if (base_units / 2 >= want && 2u * tb <= 32768u) P.nbg = 2;
-  } else if (base_units >= 148 * 32 && 2u * tb <= 32768u) {
-    P.nbg = 2;  // horizontal: small CTAs, many per SM
+  uint32_t smem = 0;
+  for (;;) {  // shrink a (knob-requested) group, then the ring, until the layout fits
+    P.tcols = 32;
+    while (P.tcols < 16u * P.nbg) P.tcols *= 2;
+    P.wbytes = (P.nbg * tb + 127u) & ~127u;
+    P.off_w = P.nring * apass::kSlot;
+    P.off_out = (P.off_w + 2 * P.wbytes + 1023u) & ~1023u;
+    P.off_bar = P.off_out + ((128u * 16u * P.nbg * oes + 1023u) & ~1023u);
+    smem = P.off_bar + 256u + 1024u;
+    if (smem <= 232448u) break;
+    if (P.nbg > 1)
+      --P.nbg;
+    else if (P.nring > 1)
+      --P.nring;
+    else
+      return set_error(TS_ERR_UNSUPPORTED, "axis_pass: window %d too large", a->K);
   }
-  if (const char* f = std::getenv("TSB_APASS_NBG")) P.nbg = std::atoi(f) > 0 ? std::atoi(f) : 1;
-  if (P.nbg > P.nb) P.nbg = P.nb;
   P.ngroups = (P.nb + P.nbg - 1) / P.nbg;
-  P.tmem_cols = 32;
-  while (P.tmem_cols < 16u * P.nbg) P.tmem_cols *= 2;
   const int64_t units = static_cast<int64_t>(planes) * P.ngroups * P.nstrip;
   if (units > 0x7FFFFFFF) return set_error(TS_ERR_UNSUPPORTED, "axis_pass: too many blocks");
   P.nunits = static_cast<int>(units);
-  {
-    const int kslots = dim == 0 ? apass::Ring<true>::kSlots : apass::Ring<false>::kSlots;
-    const int ksteps = dim == 0 ? apass::Ring<true>::kSteps : apass::Ring<false>::kSteps;
-    const int per_block = (a->K / 16 + ksteps - 1) / ksteps;
-    // vertical: 4 of the 6 slots; horizontal: one 64-column slot (the
-    // short-lived CTAs then fit ~7 per SM, which keeps more loads in flight
-    // than a deeper ring per CTA)
-    P.nring = dim == 0 ? 4 : 1;
-    if (const char* f = std::getenv("TSB_APASS_RING")) P.nring = std::atoi(f);
-    if (P.nring > P.nbg * per_block) P.nring = P.nbg * per_block;
-    if (P.nring < 1) P.nring = 1;
-    if (P.nring > kslots) P.nring = kslots;
-  }
-  P.off_b = P.nring * (dim == 0 ? apass::Ring<true>::kSlot : apass::Ring<false>::kSlot);
-  P.off_out = P.off_b + ((static_cast<uint32_t>(P.nbg) * tb + 1023u) & ~1023u);
-  P.off_bar = P.off_out + ((128u * 16u * P.nbg * oes + 1023u) & ~1023u);
-  const uint32_t smem = P.off_bar + 256u + 1024u;
+  // CTAs per SM from shared memory, TMEM (two accumulators each) and threads
+  int per_sm = static_cast<int>((228u * 1024u) / (smem + 1024u));
+  per_sm = std::min(per_sm, static_cast<int>(512u / (2u * P.tcols)));
+  per_sm = std::max(1, std::min(per_sm, 2048 / apass::kThreads));
+  const int grid = static_cast<int>(std::min<int64_t>(units, per_sm * sm_count_current()));
+
   CUtensorMap tin, tout;
-  ts_status st;
-  if (dim == 0)
-    st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs, in_ps,
-                        64, 16, CU_TENSOR_MAP_SWIZZLE_128B);
-  else
-    st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs, in_ps,
-                        64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ts_status st = encode_tmap_3d(&tin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, in, W, H, planes, in_rs,
+                                in_ps, 64, dim == 0 ? 64 : 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TS_OK) return st;
   const CUtensorMapDataType odt =
       out_dtype == TS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -325,16 +395,14 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
                       dim == 0 ? 128 : 16 * P.nbg, dim == 0 ? 16 * P.nbg : 128,
                       CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TS_OK) return st;
+  const bool epi = ep != nullptr;
   cudaError_t e;
   if (dim == 0)
-    e = out_dtype == TS_BF16
-            ? apass::launch<true, __nv_bfloat16>(P, tin, tout, smem, stream, ep != nullptr)
-            : apass::launch<true, float>(P, tin, tout, smem, stream, ep != nullptr);
+    e = epi ? apass::launch_t<true, true>(out_dtype, P, tin, tout, grid, smem, stream)
+            : apass::launch_t<true, false>(out_dtype, P, tin, tout, grid, smem, stream);
   else
-    e = out_dtype == TS_BF16
-            ? apass::launch<false, __nv_bfloat16>(P, tin, tout, smem, stream, ep != nullptr)
-            : apass::launch<false, float>(P, tin, tout, smem, stream, ep != nullptr);
-  if (e == cudaSuccess) e = cudaGetLastError();
+    e = epi ? apass::launch_t<false, true>(out_dtype, P, tin, tout, grid, smem, stream)
+            : apass::launch_t<false, false>(out_dtype, P, tin, tout, grid, smem, stream);
   return e == cudaSuccess ? TS_OK : cuda_error(e, "axis_pass launch");
 }
 
