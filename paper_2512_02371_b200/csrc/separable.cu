@@ -731,11 +731,31 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
   auto tab_of = [](const ts_axis* a, int m) -> const std::vector<int32_t>& {
     return m <= 1 ? a->tab : axis_merged(a, m)->tab;
   };
+  // operand rows / columns one tile's MMAs read: every (super-)block's K
+  // window measured from the tile's first window start.  A merged window
+  // spans the largest K_m of the axis, so a tile's last super-block can
+  // reach past the unmerged span — the stage and the V tile must cover it
+  // (else those MMA rows read neighbouring shared memory, times zero
+  // weights: NaN if that memory holds a NaN pattern)
+  auto tile_span = [](const ts_axis* a, int m, int per_tile, int ntiles) {
+    const std::vector<int32_t>& ws = m <= 1 ? a->ws : axis_merged(a, m)->ws;
+    const int K = m <= 1 ? a->K : axis_merged(a, m)->K;
+    const int n = static_cast<int>(ws.size());
+    int need = 0;
+    for (int t = 0; t < ntiles && t * per_tile < n; ++t)
+      for (int k = 0; k < per_tile && t * per_tile + k < n; ++k)
+        need = std::max(need, ws[t * per_tile + k] + K - ws[t * per_tile]);
+    return need;
+  };
+  P.nrt = (ra->nb + kRowBlocksPerTile - 1) / kRowBlocksPerTile;
+  auto row_span_of = [&](int m) {
+    return (tile_span(ra, m, kRowBlocksPerTile / m, P.nrt) + 15) / 16 * 16;
+  };
   P.m1 = choose_merge(ra, kRowBlocksPerTile);
+  if (P.m1 > 1 && row_span_of(P.m1) > kMaxRowSpan) P.m1 = 1;
   P.sb1 = kRowBlocksPerTile / P.m1;
   P.r = dev_of(ra, P.m1);
-  P.R1 = ra->row_span;
-  P.nrt = (ra->nb + kRowBlocksPerTile - 1) / kRowBlocksPerTile;
+  P.R1 = row_span_of(P.m1);
   P.planes = planes;
   // widest column tile (most output blocks per staged V tile) that fits
   // smem; at each width try the chosen super-block merges first, then
@@ -751,10 +771,13 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
       P.m1 = m1;
       P.sb1 = kRowBlocksPerTile / m1;
       P.r = dev_of(ra, m1);
+      P.R1 = row_span_of(m1);
       P.nb2 = nb2;
       P.m2 = m2;
       P.sb2 = nb2 / m2;
       P.c = dev_of(ca, m2);
+      P.nct = (ca->nb + nb2 - 1) / nb2;
+      if (tile_span(ca, m2, P.sb2, P.nct) > kColTile) continue;  // windows past the V tile
       const std::vector<int32_t>& tr = tab_of(ra, m1);
       const std::vector<int32_t>& tc = tab_of(ca, m2);
       const int ntr = static_cast<int>(tr.size()), ntc = static_cast<int>(tc.size());
@@ -764,7 +787,6 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
         for (int i = 0; i < ntr; ++i) P.tab[i] = tr[i];
         for (int i = 0; i < ntc; ++i) P.tab[ntr + i] = tc[i];
       }
-      P.nct = (ca->nb + nb2 - 1) / nb2;
       P.ntiles = planes * P.nrt * P.nct;
       if (plan_smem(P, oes)) return TS_OK;
     }
