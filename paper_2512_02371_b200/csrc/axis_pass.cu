@@ -122,6 +122,8 @@ __global__ void __launch_bounds__(kThreads, 4)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the previous kernel in the stream (e.g. the other pass) is complete
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -302,8 +304,8 @@ static cudaError_t launch(const Params& P, const CUtensorMap& tin, const CUtenso
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr_done[dev] = true;
   }
-  k<<<grid, kThreads, smem, stream>>>(tin, tout, P);
-  return cudaGetLastError();
+  const cudaError_t e = launch_pdl(k, grid, kThreads, smem, stream, tin, tout, P);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <bool VERT, bool EPI>

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <string>
 #include <atomic>
 #include <vector>
@@ -62,6 +64,31 @@ inline uint64_t next_axis_uid() {
   static std::atomic<uint64_t> n{1};
   return n.fetch_add(1);
 }
+// Launch with programmatic stream serialization (PDL): the kernel's CTAs may
+// be scheduled while the previous kernel in the stream finishes, running
+// their prologue (barrier init, TMEM allocation) until pdl_wait().  Every
+// image kernel calls pdl_wait() before touching global memory and
+// pdl_launch_dependents() right after.  TSB_PDL=0 launches plainly.
+template <typename... Exp, typename... Act>
+inline cudaError_t launch_pdl(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Act&&... args) {
+  static const bool on = [] {
+    const char* e = std::getenv("TSB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
+
 }  // namespace tsb
 
 struct ts_axis {

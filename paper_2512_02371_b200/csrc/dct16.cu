@@ -355,6 +355,8 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the previous kernel in the stream is complete
+  pdl_launch_dependents();
   // this CTA's groups: units u = blockIdx.x, += gridDim.x, each walked top
   // to bottom in groups of 8 tile rows
   const Unit ustep = unit_of(P, gridDim.x);
@@ -802,8 +804,7 @@ static cudaError_t launch_dct(const CUtensorMap& tin, const CUtensorMap& tout,
   if (e != cudaSuccess) return e;
   const int slots = G::kMinBlocks * sm_count_current();
   const int grid = P.nunits < slots ? P.nunits : slots;
-  k<<<grid, G::kThreads, G::kSmem, stream>>>(tin, tout, tout56, P);
-  return cudaSuccess;
+  return launch_pdl(k, grid, G::kThreads, G::kSmem, stream, tin, tout, tout56, P);
 }
 
 template <int BW>

@@ -206,6 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the previous kernel in the stream is complete
+  pdl_launch_dependents();
 
   const int nb2 = P.nb2;
   const int nst = static_cast<int>(L.nst);
@@ -613,8 +615,8 @@ static ts_status launch_sep_k(const SepParams& P, const CUtensorMap& tin, const 
   }
   const int sms = sm_count_current();
   const int grid = P.ntiles < sms ? P.ntiles : sms;
-  kern<<<grid, kThreads, P.L.total, stream>>>(tin, tout, P);
-  e = cudaGetLastError();
+  e = launch_pdl(kern, grid, kThreads, P.L.total, stream, tin, tout, P);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_error(e, "separable_kernel launch");
   return TS_OK;
 }

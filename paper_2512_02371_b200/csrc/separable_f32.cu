@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
     tma_load_3d(win, &tm_in, &full, S * kTC * c.tx + cbase - OFF, S * kTR * c.ty + rbase, c.p);
   };
   TileIdx cur = decompose(blockIdx.x);
+  pdl_wait();  // the previous kernel in the stream is complete
   if (tid == 0) {
     mbar_init(&full, 1);
     fence_barrier_init();
@@ -273,6 +274,10 @@ __global__ void __launch_bounds__(kThreads, T > 16 ? 2 : 3) separable_f32_kernel
   }
   __syncthreads();  // hb consumed before the next tile's horizontal pass
   }
+  // the next kernel may start only now: CTAs waiting in pdl_wait() on an SM
+  // take issue slots from this FMA-pipe-bound kernel (an early trigger
+  // halved c1's throughput)
+  pdl_launch_dependents();
 }
 
 template <int S, int T, int OFF, bool BF16, bool EXACT, bool EPI>
@@ -311,9 +316,9 @@ ts_status launch_f32(int planes, const float* in, int H, int W, int64_t irs, int
   // paired stores need 2-element aligned rows (4 B bf16 pairs / 8 B f32 pairs)
   const int vec2 = ors % 2 == 0 && ops % 2 == 0 &&
                    reinterpret_cast<uintptr_t>(out) % (BF16 ? 4 : 8) == 0;
-  fn<<<grid, kThreads, smem, st>>>(tm, H, W, ntx, nty, planes, out, OH, OW, ors, ops, vec2, rb, cb,
-                                   rw, cw, ek);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(fn, grid, kThreads, smem, st, tm, H, W, ntx, nty, planes, out, OH,
+                             OW, ors, ops, vec2, rb, cb, rw, cw, ek);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? TS_OK : cuda_error(e, "separable_f32 launch");
 }
 

@@ -120,6 +120,19 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (launch_pdl in common.h): a kernel launched
+// with programmatic stream serialization may start while the previous kernel
+// in the stream drains; pdl_wait() blocks until that kernel has completed and
+// its memory is visible (call it before the first global access that may
+// depend on it), pdl_launch_dependents() lets the next kernel start early.
+// Both are no-ops for a kernel launched without the attribute.
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // fences / named barriers
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
