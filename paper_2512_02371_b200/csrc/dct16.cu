@@ -210,27 +210,29 @@ template <int BW>
 __device__ __forceinline__ void fix_edges(uint8_t* bx, int Y, int X, int H, int W, int lane) {
   constexpr int kChunkCols = BW / 8;  // 16-byte chunks per band row
   constexpr uint32_t kHalf = kGroupRows * 128u;  // bytes per 64-column half
-  int r0[2], rs[2], nr = 0;
-  if (Y == 0) { r0[nr] = 0; rs[nr] = 8; ++nr; }
-  if (H - Y + 8 < kGroupRows) { r0[nr] = H - Y + 8; rs[nr] = H - Y + 7; ++nr; }
-  for (int e = 0; e < nr; ++e) {
-    const int rows = min(8, kGroupRows - r0[e]);
+  // (e = 0: the top / left edge, e = 1: the bottom / right edge; scalars,
+  // not small arrays, so nothing goes to local memory)
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    if (e == 0 ? Y != 0 : H - Y + 8 >= kGroupRows) continue;
+    const int r0 = e == 0 ? 0 : H - Y + 8, rs = e == 0 ? 8 : H - Y + 7;
+    const int rows = min(8, kGroupRows - r0);
     for (int idx = lane; idx < rows * kChunkCols; idx += 32) {
-      const int br = r0[e] + idx / kChunkCols, j = idx % kChunkCols, h = j >> 3, cc = j & 7;
-      const uint4 v = *reinterpret_cast<const uint4*>(bx + h * kHalf + rs[e] * 128 +
-                                                      ((cc ^ (rs[e] & 7)) << 4));
+      const int br = r0 + idx / kChunkCols, j = idx % kChunkCols, h = j >> 3, cc = j & 7;
+      const uint4 v = *reinterpret_cast<const uint4*>(bx + h * kHalf + rs * 128 +
+                                                      ((cc ^ (rs & 7)) << 4));
       *reinterpret_cast<uint4*>(bx + h * kHalf + br * 128 + ((cc ^ (br & 7)) << 4)) = v;
     }
   }
   __syncwarp();
-  int c0[2], cs[2], nc = 0;
-  if (X == 0) { c0[nc] = 0; cs[nc] = 8; ++nc; }
-  if (W - X + 8 < BW) { c0[nc] = W - X + 8; cs[nc] = W - X + 7; ++nc; }
-  for (int e = 0; e < nc; ++e) {
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    if (e == 0 ? X != 0 : W - X + 8 >= BW) continue;
+    const int c0 = e == 0 ? 0 : W - X + 8, cs = e == 0 ? 8 : W - X + 7;
     for (int br = lane; br < kGroupRows; br += 32) {
-      const uint32_t v = *reinterpret_cast<const uint16_t*>(bx + sw_off<kGroupRows>(br, cs[e]));
+      const uint32_t v = *reinterpret_cast<const uint16_t*>(bx + sw_off<kGroupRows>(br, cs));
       const uint32_t w = v | (v << 16);
-      *reinterpret_cast<uint4*>(bx + sw_off<kGroupRows>(br, c0[e])) = make_uint4(w, w, w, w);
+      *reinterpret_cast<uint4*>(bx + sw_off<kGroupRows>(br, c0)) = make_uint4(w, w, w, w);
     }
   }
   fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05 operand reads
@@ -398,8 +400,8 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
     const uint32_t c4 = (base_s + kOffC) >> 4;
     const uint64_t b3 = make_sdesc(base_s + kOffC + kCB3, 128u, 256u, kSwizzleNone);
     const uint64_t b5 = make_sdesc(base_s + kOffC + kCB5, 128u, 256u, kSwizzleNone);
-    const uint64_t b7d[2] = {make_sdesc(base_s + kOffB7, 16384u, 1024u, kSwizzle128B),
-                             make_sdesc(base_s + kOffB7 + G::kB7Bytes, 16384u, 1024u, kSwizzle128B)};
+    const uint64_t b7d0 = make_sdesc(base_s + kOffB7, 16384u, 1024u, kSwizzle128B);
+    const uint64_t b7d1 = make_sdesc(base_s + kOffB7 + G::kB7Bytes, 16384u, 1024u, kSwizzle128B);
     mbar_wait(cbar, 0);
     // S1: D1 = T · X for the group's 8 tile rows (tile k starts at group
     // buffer row 8k; lane 16k + freq).  K-step m (buffer rows 16m ..) feeds
@@ -483,11 +485,11 @@ __global__ void __launch_bounds__(Geo<BW>::kThreads, Geo<BW>::kMinBlocks)
       const bool prev = !gi.first();  // the group above is this unit's, in the other B7
       if (prev)
         mma_f16_ss_elect(tmem + kTD4, a_tmpl | (c4 + kCS7 / 16 + 15u * 16u),
-                         b7d[(i - 1) & 1] + 128u * 7, id128h, 0u);
+                         ((i - 1) & 1 ? b7d1 : b7d0) + 128u * 7, id128h, 0u);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint64_t ad = a_tmpl | (c4 + kCS7 / 16 + (14u - k) * 16u);
-        mma_f16_ss_elect(tmem + kTD4, ad, b7d[i & 1] + 128u * k, id128h,
+        mma_f16_ss_elect(tmem + kTD4, ad, (i & 1 ? b7d1 : b7d0) + 128u * k, id128h,
                          (prev || k > 0) ? 1u : 0u);
       }
       mma_commit_elect(s7done);
