@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -311,6 +312,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       trace_stamp(P, it, 2);
       const volatile int* tslot = tile_ring + 4 * (it % kTileRing);
       if (tslot[0] < 0) {  // pass the end on to epilogue 1
+        // (only once epilogue 1 has drained D_V[d]: a barrier must never run
+        // two phases ahead of its waiter, or the waiter's parity test reads
+        // the older phase as still pending — the same wait before every
+        // end-of-work signal below)
+        mbar_wait(&dv_free[d], ((it >> 1) & 1) ^ 1);
         mma_commit_elect(&dv_full[d]);
         break;
       }
@@ -359,7 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&mid_full[m], (it / nmid) & 1);
       trace_stamp(P, it, 6);
       const volatile int* tslot = tile_ring + 4 * (it % kTileRing);
-      if (tslot[0] < 0) {  // pass the end on to epilogue 2
+      if (tslot[0] < 0) {  // pass the end on to epilogue 2 (once it drained D_H)
+        mbar_wait(dh_free, (it & 1) ^ 1);
         mma_commit_elect(dh_full);
         break;
       }
@@ -406,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&dv_full[d], (it >> 1) & 1);
       if (warp == 2) trace_stamp(P, it, 4);
       if (tile_ring[4 * (it % kTileRing)] < 0) {  // pass the end on to the pass-2 issuer
+        mbar_wait(&mid_free[m], ((it / nmid) & 1) ^ 1);  // once it has read mid[m]
         mbar_arrive(&mid_full[m]);
         break;
       }
@@ -790,7 +798,17 @@ static ts_status make_params(const ts_axis* ra, const ts_axis* ca, int planes, i
         for (int i = 0; i < ntc; ++i) P.tab[ntr + i] = tc[i];
       }
       P.ntiles = planes * P.nrt * P.nct;
-      if (plan_smem(P, oes)) return TS_OK;
+      if (plan_smem(P, oes)) {
+        if (std::getenv("TSB_PLAN_VERBOSE"))  // the chosen plan, for debugging
+          fprintf(stderr,
+                  "separable plan: m1 %d sb1 %d K1 %d R1 %d | nb2 %d m2 %d sb2 %d K2 %d | ntiles r %d "
+                  "c %d tb %d %d | nst %u nmid %u res %u off_w %u off_mid %u off_out %u off_bar %u "
+                  "total %u\n",
+                  P.m1, P.sb1, P.r.K, P.R1, P.nb2, P.m2, P.sb2, P.c.K, P.r.ntiles, P.c.ntiles,
+                  P.r.tile_bytes, P.c.tile_bytes, P.L.nst, P.L.nmid, P.L.resident, P.L.off_w,
+                  P.L.off_mid, P.L.off_out, P.L.off_bar, P.L.total);
+        return TS_OK;
+      }
     }
   }
   return set_error(TS_ERR_UNSUPPORTED, "separable: tile (R1=%d) does not fit smem", P.R1);

@@ -80,3 +80,36 @@ def test_f32_input_and_output():
     yb = pipelines.downsample2x(x.bfloat16(), out_dtype=torch.float32)
     torch.cuda.synchronize()
     assert (y - yb).abs().max().item() <= 8e-3
+
+
+def test_end_of_work_signals_never_run_two_phases_ahead():
+    """Regression (found by tools/fuzz_pipelines.py): a plan with one V
+    buffer (3 x 906 x 1374, 3 / 19-tap Gaussians, f32 out: merged axes, 48 KB
+    of f32 staging) where CTAs process three tiles.  The end-of-work
+    sentinel used to pass each hand-off barrier without waiting for its
+    'free' twin, so with a slow epilogue a barrier completed two phases
+    before its waiter looked and the waiter's parity test blocked forever
+    (the mbarrier watchdog turned it into a launch failure after 4 s).  Run
+    in a subprocess: a hang must not take this test process's context."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import torch
+from paper_2512_02371_b200 import filters, pipelines
+from oracle import pipelines_ref
+import numpy as np
+g = torch.Generator(device="cpu").manual_seed(3)
+x = torch.rand((3, 906, 1374), generator=g).bfloat16()
+kv, kh = filters.gaussian_taps(3), filters.gaussian_taps(19)
+for od in (torch.float32, torch.bfloat16):
+    y = pipelines.filter_separable(x.cuda(), kv, kh, out_dtype=od).float().cpu().numpy()
+    ref = pipelines_ref.separable(x.float().numpy(), pipelines_ref.centred_axis(906, kv),
+                                  pipelines_ref.centred_axis(1374, kh))
+    assert np.abs(y - ref).max() <= 1e-2
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=root)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr

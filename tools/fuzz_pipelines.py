@@ -101,10 +101,14 @@ for i in range(N):
             xb = torch.from_numpy(x).bfloat16()
             xr = xb.float().numpy()
             thr = float(rng.uniform(0.01, 0.4))
-            desc = f"dct soft {planes}x{H}x{W} thr {thr:.3f} ep={ep}"
-            want = epi(ref.dct_denoise(xr, thr, "soft"), ep)
-            got = poisoned(lambda: pipelines.denoise_dct16(xb.cuda(), thr, "soft",
+            mode = "hard" if rng.random() < 0.5 else "soft"
+            desc = f"dct {mode} {planes}x{H}x{W} thr {thr:.3f} ep={ep}"
+            want = epi(ref.dct_denoise(xr, thr, mode), ep)
+            got = poisoned(lambda: pipelines.denoise_dct16(xb.cuda(), thr, mode,
                                                            out_dtype=odt, **kw))
+            if mode == "hard":  # pixels of tiles with a coefficient within EPS_FWD of thr
+                excused = ref.dct_flip_mask(xr, thr, 1e-5)   # may flip (tests/test_gpu_dct.py)
+                want = np.where(excused, got, want)
         counts[op] = counts.get(op, 0) + 1
         if got.shape != want.shape:
             fails.append(f"{desc}: shape {got.shape} vs {want.shape}")
@@ -115,7 +119,10 @@ for i in range(N):
             if e > tol:
                 fails.append(f"{desc}: max err {e:.4g} > {tol}")
     except Exception as ex:  # noqa: BLE001 — report and continue
-        fails.append(f"{desc}: {type(ex).__name__}: {ex}")
+        fails.append(f"{desc}: {type(ex).__name__}: {str(ex).splitlines()[0]}")
+        if "CUDA error" in str(ex):  # the context is gone: stop at the first one
+            print(f"case {i}: {fails[-1]}", flush=True)
+            break
 for f in fails:
     print("FAIL", f)
 print(f"{N} cases {counts}, {len(fails)} failures, {time.time() - t0:.0f} s")
