@@ -58,8 +58,11 @@ def test_row_bands_match_full_image(bands, shape, out):
     torch.cuda.synchronize()
     assert got.shape == full.shape
     d = (got - full).abs().max().item()
-    # same bf16 weights and window alignment; only tensor-core summation
-    # grouping at super-block boundaries can differ
+    # same bf16 weights and window alignment; only the f32 summation grouping
+    # can differ (a band may get another super-block plan than the whole
+    # image), which can flip the bf16 rounding of an intermediate V value —
+    # up to ~1 bf16 ulp of V in general (tools/fuzz_paths.py); these three
+    # geometries keep identical plans
     assert d <= 1e-5, d
 
 
