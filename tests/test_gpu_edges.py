@@ -189,3 +189,22 @@ def test_f32_kernel_more_planes_than_a_grid_dimension():
         pipelines.F32_EXACT = exact
     ref = pipelines_ref.resample(x.numpy(), 4, 8)
     assert np.array_equal(y.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("shape,oh,ow", [
+    ((1, 64, 40000), 32, 20000),    # columns past the fused kernel's packed +-32K tables
+    ((1, 40000, 64), 20000, 32),    # rows likewise
+    ((1, 70000, 48), 3000, 48),     # a 23x row factor on a very tall image
+    ((1, 16384, 16384), 1000, 1000),  # 512 MB plane through the axis passes
+])
+def test_extreme_image_sizes_match_oracle(shape, oh, ow):
+    import numpy as np
+    import torch
+    from oracle import pipelines_ref
+    from paper_2512_02371_b200 import pipelines
+    g = torch.Generator(device="cpu").manual_seed(sum(shape))
+    x = torch.rand(shape, generator=g).bfloat16()
+    y = pipelines.resample(x.cuda(), oh, ow, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    ref = pipelines_ref.resample(x.float().numpy(), oh, ow)
+    assert np.abs(y.cpu().numpy() - ref).max() <= 1e-2
