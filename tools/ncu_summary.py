@@ -18,7 +18,12 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
         "sm__cycles_elapsed.avg", "smsp__inst_executed.sum", "launch__registers_per_thread",
-        "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active"]
+        "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        # tensor pipe (tcgen05) and TMEM activity; ncu 2025 prefixes these with their section
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active"]
 
 
 def raw(report):
@@ -30,8 +35,9 @@ def raw(report):
     for vals in rows[2:]:
         d = {}
         for h, u, v in zip(hdr, units, vals):
-            if h in KEYS or h == "Kernel Name":
-                d[h] = (v, u)
+            name = h.split(".", 2)[-1] if h.split(".")[0] in ("TPC", "SM_C", "GPC", "SM_A") else h
+            if name in KEYS or h == "Kernel Name":
+                d[name] = (v, u)
         res.append(d)
     return res
 
