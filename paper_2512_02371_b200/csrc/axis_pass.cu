@@ -123,7 +123,6 @@ __global__ void __launch_bounds__(kThreads, 4)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // the previous kernel in the stream (e.g. the other pass) is complete
-  pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -290,6 +289,10 @@ __global__ void __launch_bounds__(kThreads, 4)
     tc_fence_after();
     tmem_dealloc_n(tmem, 2 * P.tcols);
   }
+  // the next kernel in the stream may launch only now: CTAs parked in
+  // griddepcontrol.wait beside working ones slowed them (an early
+  // trigger cost 30% on a 4K -> 540p two-pass resample)
+  pdl_launch_dependents();
 }
 
 template <bool VERT, typename OutT, bool EPI>

@@ -208,7 +208,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // the previous kernel in the stream is complete
-  pdl_launch_dependents();
 
   const int nb2 = P.nb2;
   const int nst = static_cast<int>(L.nst);
@@ -501,6 +500,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+  // the next kernel in the stream may launch only now: CTAs parked in
+  // griddepcontrol.wait beside working ones slowed them (an early
+  // trigger cost 30% on a 4K -> 540p two-pass resample)
+  pdl_launch_dependents();
   // the last CTA out resets the claim counters for the next launch on this
   // stream (launches on one stream are ordered; streams get their own pair)
   if (threadIdx.x == 0 && P.tile_next != nullptr) {
