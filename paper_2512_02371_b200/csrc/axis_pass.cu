@@ -357,7 +357,10 @@ ts_status axis_pass_run(const ts_axis* a, int dim, int planes, int H, int W, con
   // 4K -> 540p, 48 planes (K4)
   const bool wide = a->K >= 128;
   P.nbg = wide ? 1 : 2;
-  P.nring = wide ? 3 : 2;
+  // (a vertical pass with K >= 96 streams two slots per block: a third slot
+  // keeps its loads going — 2048^2 -> 450^2 and 4K -> 540p vertical passes
+  // 1% faster; the horizontal passes gain nothing from it)
+  P.nring = wide || (dim == 0 && a->K >= 96) ? 3 : 2;
   if (const char* f = std::getenv("TSB_APASS_NBG")) P.nbg = std::max(1, std::atoi(f));
   if (const char* f = std::getenv("TSB_APASS_RING")) P.nring = std::atoi(f);
   P.nbg = std::min(std::min(P.nbg, 8), P.nb);
